@@ -1,0 +1,125 @@
+/*
+ * tc_collectives.h -- C ABI of the B200 (sm_100a) tensor-core segmented
+ * reduction and scan library (arXiv 1811.09736, re-designed for Blackwell).
+ *
+ * The reference (`halftile`, /root/reference/pkg) is a pure-Python package
+ * with no FFI.  Each entry point below replaces the body of one reference
+ * operator; the Python shim in paper_1811_09736_b200/ keeps the reference
+ * signatures and validation and calls these through ctypes:
+ *
+ *   tc_seg_reduce  <- halftile.reduce.segmented_reduce  (reduce.py:379-446)
+ *                     and the warp/block primitives it dispatches to:
+ *                     reduce_16 (:92), reduce_256 (:109),
+ *                     reduce_256n_efficient (:123), reduce_256n_inefficient
+ *                     (:144), reduce_16n_strided (:171),
+ *                     reduce_16n_coalesced (:201), block_reduce_256n (:278)
+ *   tc_full_reduce <- halftile.reduce.grid_reduce       (reduce.py:332-373)
+ *   tc_seg_scan    <- halftile.scan.segmented_scan      (scan.py:316-388)
+ *                     and scan_16 (:58), scan_256/_256n (:94-119),
+ *                     scan_16n (:122), block_scan_256n (:178)
+ *   tc_full_scan   <- halftile.scan.grid_scan           (scan.py:249-310)
+ *
+ * Conventions
+ *   - All data pointers are DEVICE pointers owned by the caller; the library
+ *     never retains or frees them.  Calls are stream-ordered (no host sync)
+ *     and reentrant across host threads on different streams, each with its
+ *     own workspace.
+ *   - Input is IEEE binary16, contiguous, 16-byte aligned, 0 < n < 2^37.
+ *   - Segment semantics follow halftile.segmented.pad_segmented
+ *     (segmented.py:57-89): segment k covers elements [k*seg, (k+1)*seg),
+ *     the last segment may be ragged (shorter); a reduce returns
+ *     ceil(n/seg) sums, a scan returns n prefix sums.
+ *   - Arithmetic: products on the tensor core (tcgen05.mma kind::f16, fp32
+ *     accumulation in TMEM), cross-row / cross-tile carries in fp32 / fp64,
+ *     one rounding to the output dtype.  This is never less precise than the
+ *     reference TileEngine.mma model (engine.py:326-348).
+ *   - Argument errors are detected on the host before any launch and leave
+ *     `out` untouched.  Status codes map 1:1 onto the reference exceptions:
+ *     TC_BAD_LENGTH -> halftile.errors.BadLengthError, TC_BAD_CONFIG ->
+ *     BadConfigError (errors.py:29-38).
+ *   - `ws` is a caller-owned device workspace of at least
+ *     tc_workspace_bytes(op, n, seg) bytes.  It MUST be zero-filled once at
+ *     allocation; the kernels leave it in a reusable state.  One workspace
+ *     must not be used by two in-flight calls at the same time.
+ */
+#ifndef TC_COLLECTIVES_H
+#define TC_COLLECTIVES_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define TC_OK 0
+#define TC_BAD_LENGTH 1        /* -> BadLengthError (errors.py:29) */
+#define TC_BAD_CONFIG 2        /* -> BadConfigError (errors.py:33) */
+#define TC_BAD_ALIGNMENT 3     /* pointer not 16-byte aligned      */
+#define TC_WORKSPACE_TOO_SMALL 4
+#define TC_CUDA_ERROR 5        /* -> RuntimeError + tc_last_error() */
+#define TC_NO_DEVICE 6         /* no sm_100 device / driver entry point */
+
+/* output dtypes (engine.acc_dtype, engine.py:244-246: half | single) */
+#define TC_F16 0
+#define TC_F32 1
+#define TC_F64 2               /* reduce only: fp64 partial for NCCL combine */
+
+/* op ids for tc_workspace_bytes */
+#define TC_OP_REDUCE 0
+#define TC_OP_SCAN 1
+
+/* Bytes of device workspace an op over n elements with segment size seg
+ * needs (seg >= n means one segment: the grid/full variants). */
+size_t tc_workspace_bytes(int op, int64_t n, int64_t seg);
+
+/* Segmented sum: out[k] = sum(x[k*seg : min((k+1)*seg, n)]) for
+ * k < ceil(n/seg), stored as out_dtype (TC_F16 | TC_F32 | TC_F64).
+ * Replaces segmented_reduce (reduce.py:379). */
+int tc_seg_reduce(const void* x, int64_t n, int64_t seg, void* out,
+                  int out_dtype, void* ws, size_t ws_bytes, void* stream);
+
+/* Full sum of n elements into out[0] (one output).  Replaces grid_reduce
+ * (reduce.py:332).  Equivalent to tc_seg_reduce with seg = n. */
+int tc_full_reduce(const void* x, int64_t n, void* out, int out_dtype,
+                   void* ws, size_t ws_bytes, void* stream);
+
+/* Segmented inclusive (exclusive != 0: exclusive) prefix sum, n outputs in
+ * out_dtype (TC_F16 | TC_F32).  Replaces segmented_scan (scan.py:316); the
+ * exclusive form equals the reference's shift-right-and-inject-zero
+ * (scan.py:332-341).
+ *   carry_in  (nullable, DEVICE, 1 double): the first segment continues a
+ *             segment begun before x[0] whose running sum is *carry_in
+ *             (cross-GPU carry of a sharded full scan).
+ *   total_out (nullable, DEVICE, 1 double): receives the inclusive running
+ *             sum of the last (open) segment, i.e. carry_in + sum(x) when
+ *             seg >= n. */
+int tc_seg_scan(const void* x, int64_t n, int64_t seg, void* out,
+                int out_dtype, int exclusive, const double* carry_in,
+                double* total_out, void* ws, size_t ws_bytes, void* stream);
+
+/* Full (one-segment) scan.  Replaces grid_scan (scan.py:249). */
+int tc_full_scan(const void* x, int64_t n, void* out, int out_dtype,
+                 int exclusive, const double* carry_in, double* total_out,
+                 void* ws, size_t ws_bytes, void* stream);
+
+/* Human-readable name of a status code. */
+const char* tc_status_string(int status);
+
+/* Detail message of the last failing call on this host thread ("" if none). */
+const char* tc_last_error(void);
+
+/* Number of kernel launches issued by this host thread since the last call
+ * to tc_reset_launch_count (used by bench.py's gpu_launches claim). */
+uint64_t tc_launch_count(void);
+void tc_reset_launch_count(void);
+
+/* ABI version: (major << 16) | minor. */
+int tc_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TC_COLLECTIVES_H */

@@ -1,0 +1,127 @@
+"""Device-side entry points: torch CUDA tensors in, torch CUDA tensors out.
+
+Thin wrappers over the C ABI (include/tc_collectives.h): they own output
+and workspace allocation on the caller's current CUDA stream and map status
+codes onto the reference's exceptions (BadLengthError / BadConfigError,
+pkg/src/halftile/errors.py:29-38).  Everything is stream-ordered; nothing
+here synchronises.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .errors import BadConfigError, BadLengthError
+
+_DT = {torch.float16: _lib.TC_F16, torch.float32: _lib.TC_F32, torch.float64: _lib.TC_F64}
+
+_ws_cache: dict = {}
+
+
+def _check(rc: int) -> None:
+    if rc == _lib.TC_OK:
+        return
+    msg = _lib.last_error()
+    if rc == _lib.TC_BAD_LENGTH:
+        raise BadLengthError(msg)
+    if rc == _lib.TC_BAD_CONFIG:
+        raise BadConfigError(msg)
+    raise RuntimeError(f"tc_collectives: {_lib.status_string(rc)}: {msg}")
+
+
+def _stream_ptr(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def workspace(op: int, n: int, seg: int, device: torch.device) -> torch.Tensor:
+    """Zero-initialised workspace cached per (device, stream); grows on demand.
+
+    The kernels leave a workspace reusable (ticket reset, epoch-tagged
+    look-back flags), so one allocation serves every later call on that
+    stream."""
+    need = int(_lib.lib.tc_workspace_bytes(op, n, seg))
+    key = (device.index, _stream_ptr(device))
+    ws = _ws_cache.get(key)
+    if ws is None or ws.numel() < need:
+        size = max(need, 1 << 20)
+        if ws is not None:
+            size = max(size, 2 * ws.numel())
+        ws = torch.zeros(size, dtype=torch.uint8, device=device)
+        _ws_cache[key] = ws
+    return ws
+
+
+def _prep(x: torch.Tensor) -> torch.Tensor:
+    if not x.is_cuda:
+        raise ValueError("device entry points take CUDA tensors")
+    if x.dim() != 1:
+        raise BadLengthError("collectives operate on flat vectors")
+    if x.dtype != torch.float16:
+        x = x.to(torch.float16)
+    if not x.is_contiguous() or x.data_ptr() % 16:
+        x = x.contiguous().clone()
+    return x
+
+
+def seg_reduce(x: torch.Tensor, seg: int, out_dtype=torch.float16, out=None) -> torch.Tensor:
+    """ceil(n/seg) segment sums of a CUDA fp16 vector (tc_seg_reduce)."""
+    x = _prep(x)
+    n = x.numel()
+    if n == 0:
+        raise BadLengthError("input must be a non-empty flat vector")
+    if seg < 1:
+        raise BadLengthError(f"segment size must be positive, got {seg}")
+    nseg = -(-n // seg)
+    if out is None:
+        out = torch.empty(nseg, dtype=out_dtype, device=x.device)
+    ws = workspace(_lib.TC_OP_REDUCE, n, seg, x.device)
+    _check(_lib.lib.tc_seg_reduce(x.data_ptr(), n, seg, out.data_ptr(), _DT[out.dtype],
+                                  ws.data_ptr(), ws.numel(), _stream_ptr(x.device)))
+    return out
+
+
+def full_reduce(x: torch.Tensor, out_dtype=torch.float16, out=None) -> torch.Tensor:
+    """Sum of all n elements as a 1-element tensor (tc_full_reduce)."""
+    x = _prep(x)
+    n = x.numel()
+    if n == 0:
+        raise BadLengthError("input must be a non-empty flat vector")
+    if out is None:
+        out = torch.empty(1, dtype=out_dtype, device=x.device)
+    ws = workspace(_lib.TC_OP_REDUCE, n, n, x.device)
+    _check(_lib.lib.tc_full_reduce(x.data_ptr(), n, out.data_ptr(), _DT[out.dtype],
+                                   ws.data_ptr(), ws.numel(), _stream_ptr(x.device)))
+    return out
+
+
+def seg_scan(x: torch.Tensor, seg: int, out_dtype=torch.float16, exclusive=False,
+             carry_in: torch.Tensor | None = None, total_out: torch.Tensor | None = None,
+             out=None) -> torch.Tensor:
+    """Segmented inclusive/exclusive prefix sums (tc_seg_scan).
+
+    ``carry_in`` / ``total_out`` are optional 1-element float64 CUDA tensors
+    (cross-GPU carry of a sharded full scan)."""
+    x = _prep(x)
+    n = x.numel()
+    if n == 0:
+        raise BadLengthError("input must be a non-empty flat vector")
+    if seg < 1:
+        raise BadLengthError(f"segment size must be positive, got {seg}")
+    if out is None:
+        out = torch.empty(n, dtype=out_dtype, device=x.device)
+    ws = workspace(_lib.TC_OP_SCAN, n, seg, x.device)
+    cin = carry_in.data_ptr() if carry_in is not None else None
+    tout = total_out.data_ptr() if total_out is not None else None
+    _check(_lib.lib.tc_seg_scan(x.data_ptr(), n, seg, out.data_ptr(), _DT[out.dtype],
+                                1 if exclusive else 0, cin, tout, ws.data_ptr(), ws.numel(),
+                                _stream_ptr(x.device)))
+    return out
+
+
+def full_scan(x: torch.Tensor, out_dtype=torch.float16, exclusive=False,
+              carry_in: torch.Tensor | None = None, total_out: torch.Tensor | None = None,
+              out=None) -> torch.Tensor:
+    """One-segment scan of the whole vector (tc_full_scan)."""
+    x = _prep(x)
+    return seg_scan(x, max(x.numel(), 1), out_dtype, exclusive, carry_in, total_out, out)

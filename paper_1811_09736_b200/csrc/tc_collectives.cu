@@ -1,0 +1,1065 @@
+// tc_collectives.cu -- B200 (sm_100a) tensor-core segmented reduction and
+// scan (arXiv 1811.09736), behind the C ABI in include/tc_collectives.h.
+//
+// Design (see DESIGN.md for the full story):
+//
+//  * Data view.  The fp16 input is a row-major matrix X[R x 64] (one row =
+//    128 B = one SW128 swizzle atom).  A tile is 128 consecutive rows
+//    (8192 elements, 16 KB, contiguous in HBM) loaded by one TMA box into a
+//    multi-stage shared-memory ring.  Rows past n are zero-filled by TMA;
+//    the ragged last row (n % 64 elements) is patched in the epilogue.
+//
+//  * Tensor-core formulation (the paper's "reduction = P.A.Q, scan = A.U +
+//    L.(carries).U").  With granule g = gcd(seg, 64) and GR = 64/g granules
+//    per row, one tcgen05.mma chain (M=128, K=64 as 4 x K16) computes
+//        reduce: D[128 x N] = X_tile . B_g   (B_g[k][j] = [k/g == j])
+//                -> D[r][j] = sum of granule j of row r   (the A.Q step)
+//        scan:   D[128 x 64] = X_tile . U_g  (U_g block-diagonal upper-
+//                triangular ones with g x g blocks) -> in-granule inclusive
+//                prefix sums of every row            (the A.U step)
+//    with fp16 operands from SMEM descriptors and fp32 accumulators in TMEM.
+//    The P-side / L-side combine (across granules, rows, tiles, CTAs) is
+//    the carry chain: a segmented (value, flag) scan in registers, warp
+//    shuffles across the 32 rows of a warp, shared memory across the four
+//    epilogue warps, registers across a CTA's tiles (reduce) and a
+//    decoupled look-back over tiles (scan), all in fp32/fp64.
+//
+//  * Warp specialisation (192 threads, persistent grid): warp 0 = TMA
+//    producer, warp 1 = TMEM allocator + single-thread MMA issuer, warps
+//    2..5 = epilogue (TMEM lane quadrant = warp % 4).  mbarrier rings:
+//    full/empty (TMA <-> MMA) and tmem_full/tmem_empty (MMA <-> epilogue).
+//
+//  * Scan outputs are staged through swizzled shared memory and written by
+//    TMA stores; reduce outputs are written with plain coalesced stores.
+//
+// Reference correspondence (pkg/src/halftile):
+//    reduce granule sums     reduce.py:92-106 (Reduction16 P.A), :171-198
+//    row/tile/CTA combine    reduce.py:123-141, :278-326, :332-373
+//    scan in-granule A.U     scan.py:58-71, :74-91 (RowScan)
+//    carry chain             scan.py:102-119, :155-172, :178-243, :249-310
+//    padding semantics       segmented.py:57-89
+//    MMA numerics            engine.py:326-348 (products exact, one rounding)
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+
+#include "sm100_ptx.cuh"
+#include "tc_collectives.h"
+
+namespace tc {
+
+constexpr int kRow = 64;                              // elements per row
+constexpr int kTileRows = 128;                        // UMMA M
+constexpr int kTileElems = kRow * kTileRows;          // 8192
+constexpr uint32_t kTileBytes = kTileElems * 2;       // 16 KB of fp16
+constexpr int kThreads = 192;                         // 6 warps
+constexpr int kEpiThreads = 128;                      // warps 2..5
+constexpr int kEpiBar = 1;                            // named barrier id
+constexpr int OP_REDUCE = 0;
+constexpr int OP_SCAN = 1;
+constexpr int kMaxCtas = 1024;                        // persistent grid cap
+constexpr unsigned kFull = 0xffffffffu;
+
+struct WsHeader {
+  unsigned int ticket;
+  unsigned int epoch;
+  unsigned int pad[62];
+};
+struct Entry {  // one cross-CTA partial of a reduce
+  long long seg;
+  double val;
+};
+// workspace layout
+constexpr size_t kWsZeroRow = 256;   // 256 B of zeros: TMA source when R == 0
+constexpr size_t kWsDummyOut = 512;  // 512 B scratch: TMA store target when R == 0
+constexpr size_t kWsEntries = 1024;
+constexpr size_t kWsLookback = kWsEntries + sizeof(Entry) * 2 * kMaxCtas;
+
+struct Params {
+  const __half* x;
+  void* out;
+  long long n;          // elements
+  long long seg;        // segment size
+  long long m;          // granules per segment (seg / g)
+  long long rows_full;  // n / 64
+  long long num_tiles;  // ceil(n / 8192)
+  long long qlast;      // index of the last granule, (n - 1) / g
+  const double* carry_in;
+  double* total_out;
+  WsHeader* hdr;
+  Entry* entries;
+  uint32_t* lb_flag;
+  double* lb_agg;
+  double* lb_inc;
+  int exclusive;
+  int need_fixup;     // reduce: segments may straddle CTA ranges
+  int need_lookback;  // scan: segments may straddle tiles (or carry_in given)
+};
+
+template <typename T>
+__device__ __forceinline__ T cvt_out(float v);
+template <>
+__device__ __forceinline__ __half cvt_out<__half>(float v) {
+  return __float2half_rn(v);
+}
+template <>
+__device__ __forceinline__ float cvt_out<float>(float v) {
+  return v;
+}
+template <>
+__device__ __forceinline__ double cvt_out<double>(float v) {
+  return static_cast<double>(v);
+}
+// one rounding from the fp64 carry chain straight to the output dtype
+template <typename T>
+__device__ __forceinline__ T cvt_out_d(double v);
+template <>
+__device__ __forceinline__ __half cvt_out_d<__half>(double v) {
+  return __double2half(v);
+}
+template <>
+__device__ __forceinline__ float cvt_out_d<float>(double v) {
+  return __double2float_rn(v);
+}
+template <>
+__device__ __forceinline__ double cvt_out_d<double>(double v) {
+  return v;
+}
+
+__host__ __device__ constexpr int pow2_at_least(int v) {
+  return v <= 32 ? 32 : v <= 64 ? 64 : v <= 128 ? 128 : v <= 256 ? 256 : 512;
+}
+
+template <int OP, int GR, typename OutT>
+struct Cfg {
+  static constexpr int G = 64 / GR;  // granule size (elements)
+  static constexpr int N = (OP == OP_SCAN) ? 64 : (GR < 16 ? 16 : GR);  // UMMA N
+  static constexpr int STAGES = (OP == OP_SCAN && sizeof(OutT) == 4) ? 6 : 8;
+  static constexpr int ACC = 4;  // TMEM accumulator stages
+  static constexpr int TMEM_COLS = pow2_at_least(ACC * N);
+  static constexpr int OUT_BUFS = (OP == OP_SCAN) ? 2 : 0;
+  static constexpr uint32_t OUT_BYTES = kTileElems * sizeof(OutT);
+  static constexpr uint32_t OFF_B = STAGES * kTileBytes;
+  static constexpr uint32_t OFF_OUT = OFF_B + ((N * 128 + 1023) / 1024) * 1024;
+  static constexpr uint32_t OFF_MISC = OFF_OUT + OUT_BUFS * OUT_BYTES;
+  static constexpr int LD_COLS = (OP == OP_SCAN) ? 64 : GR;  // TMEM columns read per tile
+};
+
+template <int STAGES, int ACC>
+struct Misc {
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t tfull[ACC];
+  uint64_t tempty[ACC];
+  uint32_t tmem_base;
+  int is_last;
+  float pv[2][4];
+  int pf[2][4];
+  double lb_prefix[2];
+  long long head_seg;
+  double head_val;
+};
+
+template <int OP, int GR, typename OutT>
+constexpr uint32_t smem_bytes() {
+  using C = Cfg<OP, GR, OutT>;
+  return C::OFF_MISC + sizeof(Misc<C::STAGES, C::ACC>) + 1024;  // +1024: alignment slack
+}
+
+// Constant B operand, K-major, 128-B swizzled: row n (N index) holds B[k][n]
+// for k = 0..63.  Reduce: granule indicator.  Scan: block-diag upper-tri U.
+template <int OP, int GR, int N>
+__device__ void build_b(uint8_t* sb) {
+  constexpr int G = 64 / GR;
+  for (int idx = threadIdx.x; idx < N * 8; idx += blockDim.x) {
+    const int n = idx >> 3, pos = idx & 7;
+    const int lc = pos ^ (n & 7);  // logical 16-B chunk stored at physical position pos
+    __align__(16) __half h[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int k = lc * 8 + e;
+      bool one;
+      if (OP == OP_REDUCE)
+        one = (n < GR) && (k / G == n);
+      else
+        one = (k / G == n / G) && (k <= n);
+      h[e] = __float2half_rn(one ? 1.f : 0.f);
+    }
+    *reinterpret_cast<uint4*>(sb + n * 128 + pos * 16) = *reinterpret_cast<uint4*>(h);
+  }
+}
+
+// Compose segmented-sum pairs: x then y.  (flag = "a boundary occurred")
+__device__ __forceinline__ void compose(float& xv, int& xf, float yv, int yf) {
+  xv = yf ? yv : xv + yv;
+  xf |= yf;
+}
+
+// Inclusive segmented scan of (v, f) pairs across the 32 lanes of a warp.
+__device__ __forceinline__ void warp_pair_scan(float& v, int& f, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const float vu = __shfl_up_sync(kFull, v, d);
+    const int fu = __shfl_up_sync(kFull, f, d);
+    if (lane >= d) {
+      if (!f) v += vu;
+      f |= fu;
+    }
+  }
+}
+
+// Decoupled look-back over tiles: exclusive running value entering tile t.
+// Lane i inspects tile (t-1-i) - 32*w.  Status word = (epoch << 2) | state,
+// state 1 = aggregate published (lb_agg), 2 = inclusive published (lb_inc).
+__device__ double lookback(const Params& p, long long t, uint32_t ep, int lane) {
+  double acc = 0.0;
+  long long base = t - 1;
+  while (true) {
+    const long long j = base - lane;
+    bool isP = true;
+    double val = 0.0;
+    if (j >= 0) {
+      uint32_t st;
+      do {
+        st = ptx::ld_acquire_u32(p.lb_flag + j);
+      } while ((st >> 2) != ep || (st & 3u) == 0u);
+      isP = (st & 3u) == 2u;
+      val = isP ? ptx::ld_relaxed_f64(p.lb_inc + j) : ptx::ld_relaxed_f64(p.lb_agg + j);
+    }
+    const unsigned pm = __ballot_sync(kFull, isP);
+    const int lim = pm ? (__ffs(pm) - 1) : 31;
+    double c = (lane <= lim) ? val : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+    acc += c;
+    if (pm) break;
+    base -= 32;
+  }
+  return acc;
+}
+
+__device__ __forceinline__ void publish(const Params& p, long long t, uint32_t ep, int state,
+                                        double v) {
+  if (state == 2)
+    ptx::st_relaxed_f64(p.lb_inc + t, v);
+  else
+    ptx::st_relaxed_f64(p.lb_agg + t, v);
+  ptx::st_release_u32(p.lb_flag + t, (ep << 2) | static_cast<uint32_t>(state));
+}
+
+template <int OP, int GR, typename OutT>
+__global__ void __launch_bounds__(kThreads, 1)
+    seg_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+               const Params p) {
+  using C = Cfg<OP, GR, OutT>;
+  using MiscT = Misc<C::STAGES, C::ACC>;
+  constexpr int G = C::G;
+  constexpr int N = C::N;
+  constexpr int STAGES = C::STAGES;
+  constexpr int ACC = C::ACC;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem =
+      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  MiscT* misc = reinterpret_cast<MiscT*>(smem + C::OFF_MISC);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  // ---- work assignment: reduce = contiguous tile range, scan = round robin
+  const long long T = p.num_tiles;
+  const int Gc = gridDim.x;
+  const int cta = blockIdx.x;
+  long long t_begin, t_end;
+  int t_count;
+  if (OP == OP_REDUCE) {
+    t_begin = T * cta / Gc;
+    t_end = T * (cta + 1) / Gc;
+    t_count = static_cast<int>(t_end - t_begin);
+  } else {
+    t_begin = cta;
+    t_end = T;
+    t_count = static_cast<int>((T - cta + Gc - 1) / Gc);
+  }
+  auto tile_of = [&](int i) -> long long {
+    return OP == OP_REDUCE ? t_begin + i : static_cast<long long>(cta) + static_cast<long long>(i) * Gc;
+  };
+  const uint32_t ep = (p.hdr->epoch + 1u) & 0x3FFFFFFFu;
+
+  // ---- one-time setup
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tin);
+    if (OP == OP_SCAN) ptx::prefetch_tmap(&tout);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&misc->full[s], 1);
+      ptx::mbar_init(&misc->empty[s], 1);
+    }
+    for (int a = 0; a < ACC; ++a) {
+      ptx::mbar_init(&misc->tfull[a], 1);
+      ptx::mbar_init(&misc->tempty[a], kEpiThreads);
+    }
+    misc->head_seg = -1;
+    misc->head_val = 0.0;
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc(&misc->tmem_base, C::TMEM_COLS);
+    ptx::tmem_relinquish();
+  }
+  build_b<OP, GR, N>(smem + C::OFF_B);
+  ptx::fence_proxy_async_smem();  // B written by the generic proxy, read by the tensor core
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = misc->tmem_base;
+
+  if (warp == 0) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      const uint64_t pol = ptx::policy_evict_first();
+      for (int i = 0; i < t_count; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        ptx::mbar_wait(&misc->empty[s], ph ^ 1u);
+        ptx::mbar_arrive_expect_tx(&misc->full[s], kTileBytes);
+        ptx::tma_load_2d(&tin, smem + s * kTileBytes, &misc->full[s], 0,
+                         static_cast<int32_t>(tile_of(i) * kTileRows), pol);
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer (one thread) =================
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_f16_f32(128, N);
+      const uint64_t bdesc = ptx::smem_desc_sw128(smem + C::OFF_B);
+      for (int i = 0; i < t_count; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        const int a = i % ACC;
+        const uint32_t aph = (i / ACC) & 1;
+        ptx::mbar_wait(&misc->tempty[a], aph ^ 1u);
+        ptx::mbar_wait(&misc->full[s], ph);
+        ptx::tc_fence_after();
+        const uint64_t adesc = ptx::smem_desc_sw128(smem + s * kTileBytes);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)  // K = 64 = 4 x 16; +32 B per K step inside the SW128 atom
+          ptx::mma_f16_ss(tmem + a * N, adesc + 2 * k, bdesc + 2 * k, idesc, k > 0 ? 1u : 0u);
+        ptx::mma_commit(&misc->empty[s]);
+        ptx::mma_commit(&misc->tfull[a]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ================= epilogue (warps 2..5) =================
+    const int qd = warp & 3;                 // TMEM lane quadrant
+    const int rit = qd * 32 + lane;          // row in tile
+    const int et = threadIdx.x - 64;         // epilogue thread id 0..127
+    const bool leader = (et == 0);
+    const uint32_t lane_base = static_cast<uint32_t>(qd * 32) << 16;
+    const long long range_first_elem = t_begin * kTileElems;  // reduce only
+    double tile_carry = 0.0;  // reduce: open segment value entering the tile (CTA-local)
+    const bool has_carry = (p.carry_in != nullptr);
+    const double carry0 = (OP == OP_SCAN && has_carry) ? *p.carry_in : 0.0;
+
+    for (int i = 0; i < t_count; ++i) {
+      const long long t = tile_of(i);
+      const int a = i % ACC;
+      const uint32_t aph = (i / ACC) & 1;
+      const int par = i & 1;
+      ptx::mbar_wait(&misc->tfull[a], aph);
+      ptx::tc_fence_after();
+      constexpr int LD = C::LD_COLS;
+      uint32_t r[LD];
+      if constexpr (LD <= 32) {
+        ptx::tmem_ld_32x32b<LD>(tmem + lane_base + a * N, r);
+      } else {
+        uint32_t(&r0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[0]);
+        uint32_t(&r1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[32]);
+        ptx::tmem_ld_32x32b<32>(tmem + lane_base + a * N, r0);
+        ptx::tmem_ld_32x32b<32>(tmem + lane_base + a * N + 32, r1);
+      }
+      ptx::tmem_wait_ld();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&misc->tempty[a]);
+
+      const long long row = t * kTileRows + rit;
+      const long long q0 = row * GR;  // first granule of this row
+
+      if constexpr (OP == OP_REDUCE) {
+        // ---------------------------------------------------------- reduce
+        float gs[GR];
+#pragma unroll
+        for (int j = 0; j < GR; ++j) gs[j] = __uint_as_float(r[j]);
+        if (row == p.rows_full) {  // ragged last row: beyond the TMA view, patch from HBM
+          const long long e0 = row * kRow;
+#pragma unroll 1
+          for (int j = 0; j < GR; ++j) {
+            float s = 0.f;
+            for (int k = 0; k < G; ++k) {
+              const long long e = e0 + j * G + k;
+              if (e < p.n) s += __half2float(p.x[e]);
+            }
+            gs[j] = s;
+          }
+        }
+        OutT* out = reinterpret_cast<OutT*>(p.out);
+        if (p.m == 1) {
+          // every granule is a whole segment: out[q0 + j] = gs[j]
+          if (q0 + GR - 1 <= p.qlast) {
+#pragma unroll
+            for (int j = 0; j < GR; ++j) out[q0 + j] = cvt_out<OutT>(gs[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < GR; ++j)
+              if (q0 + j <= p.qlast) out[q0 + j] = cvt_out<OutT>(gs[j]);
+          }
+          continue;
+        }
+        // thread-local pass over the row's granules.  `seg` always indexes
+        // the segment containing granule q0 + j.
+        long long rem = p.m - 1 - (q0 % p.m);  // granules until the next segment end
+        long long seg = (q0 + rem) / p.m;
+        const long long seg0 = seg;            // segment closed by the row's first end
+        float run = 0.f, head = 0.f;
+        int seen = 0;
+#pragma unroll
+        for (int j = 0; j < GR; ++j) {
+          run += gs[j];
+          const long long qj = q0 + j;
+          if (qj <= p.qlast && (rem == 0 || qj == p.qlast)) {
+            if (!seen) {
+              head = run;  // needs the carry from earlier rows / tiles
+              seen = 1;
+            } else {
+              out[seg] = cvt_out<OutT>(run);  // segment wholly inside this row
+            }
+            ++seg;
+            run = 0.f;
+          }
+          rem = (rem == 0) ? p.m - 1 : rem - 1;
+        }
+        // cross-row segmented scan of (tail run, has_end)
+        float v = run;
+        int f = seen;
+        warp_pair_scan(v, f, lane);
+        float ve = __shfl_up_sync(kFull, v, 1);
+        int fe = __shfl_up_sync(kFull, f, 1);
+        if (lane == 0) {
+          ve = 0.f;
+          fe = 0;
+        }
+        if (lane == 31) {
+          misc->pv[par][qd] = v;
+          misc->pf[par][qd] = f;
+        }
+        ptx::named_bar_sync(kEpiBar, kEpiThreads);
+        float wv = 0.f, tv = 0.f;
+        int wf = 0, tf = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float yv = misc->pv[par][k];
+          const int yf = misc->pf[par][k];
+          if (k < qd) compose(wv, wf, yv, yf);
+          compose(tv, tf, yv, yf);
+        }
+        float cin = ve;
+        int cfl = fe;
+        {
+          float xv = wv;
+          int xf = wf;
+          compose(xv, xf, ve, fe);
+          cin = xv;
+          cfl = xf;
+        }
+        if (seen) {
+          const double val = static_cast<double>(cin + head) + (cfl ? 0.0 : tile_carry);
+          if (seg0 * p.seg < range_first_elem) {
+            misc->head_seg = seg0;  // partial: segment began in an earlier CTA's range
+            misc->head_val = val;
+          } else {
+            out[seg0] = cvt_out_d<OutT>(val);
+          }
+        }
+        tile_carry = tf ? static_cast<double>(tv) : tile_carry + static_cast<double>(tv);
+      } else {
+        // ------------------------------------------------------------ scan
+        float vv[64];
+#pragma unroll
+        for (int k = 0; k < 64; ++k) vv[k] = __uint_as_float(r[k]);
+        if (row == p.rows_full) {  // ragged last row: recompute in-granule scans from HBM
+          const long long e0 = row * kRow;
+          float s = 0.f;
+#pragma unroll
+          for (int k = 0; k < 64; ++k) {
+            if (k % G == 0) s = 0.f;
+            const long long e = e0 + k;
+            s += (e < p.n) ? __half2float(p.x[e]) : 0.f;
+            vv[k] = s;
+          }
+        }
+        // thread-local pass: starts, local offsets, chain-to-row-start flags
+        float off[GR];
+        int chain[GR];
+        float run = 0.f;
+        int seen = 0;
+        {
+          long long rem = (p.m - (q0 % p.m)) % p.m;  // granules until the next start
+#pragma unroll
+          for (int j = 0; j < GR; ++j) {
+            const bool st = (rem == 0) && (q0 + j <= p.qlast) && !((q0 + j) == 0 && has_carry);
+            if (st) {
+              run = 0.f;
+              seen = 1;
+            }
+            off[j] = run;
+            chain[j] = !seen;
+            run += vv[j * G + G - 1];
+            rem = (rem == 0) ? p.m - 1 : rem - 1;
+          }
+        }
+        // staging buffer reuse: the TMA store issued two tiles ago must have
+        // finished reading it before anyone writes.
+        if (leader) ptx::bulk_wait_read<1>();
+        float cin = 0.f;
+        int cfl = 1;
+        float tv = 0.f;
+        int tf = 1;
+        const bool need_rows = (p.m != 1) || has_carry || (p.total_out != nullptr);
+        if (need_rows) {
+          float v = run;
+          int f = seen;
+          warp_pair_scan(v, f, lane);
+          float ve = __shfl_up_sync(kFull, v, 1);
+          int fe = __shfl_up_sync(kFull, f, 1);
+          if (lane == 0) {
+            ve = 0.f;
+            fe = 0;
+          }
+          if (lane == 31) {
+            misc->pv[par][qd] = v;
+            misc->pf[par][qd] = f;
+          }
+          ptx::named_bar_sync(kEpiBar, kEpiThreads);
+          float wv = 0.f;
+          int wf = 0;
+          tv = 0.f;
+          tf = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float yv = misc->pv[par][k];
+            const int yf = misc->pf[par][k];
+            if (k < qd) compose(wv, wf, yv, yf);
+            compose(tv, tf, yv, yf);
+          }
+          compose(wv, wf, ve, fe);
+          cin = wv;
+          cfl = wf;
+        } else {
+          ptx::named_bar_sync(kEpiBar, kEpiThreads);
+        }
+        // tile prefix (look-back) for segments entering this tile
+        double tprefix = 0.0;
+        if (p.need_lookback) {
+          const long long tq0 = t * (long long)kTileRows * GR;  // first granule of the tile
+          const bool first_start = (tq0 % p.m == 0) && !(t == 0 && has_carry);
+          if (warp == 2) {
+            if (lane == 0) {
+              if (tf)
+                publish(p, t, ep, 2, static_cast<double>(tv));
+              else if (!(t == 0 || first_start))
+                publish(p, t, ep, 1, static_cast<double>(tv));
+            }
+            double pre;
+            if (t == 0)
+              pre = carry0;
+            else if (first_start)
+              pre = 0.0;
+            else
+              pre = lookback(p, t, ep, lane);
+            if (lane == 0) {
+              const double incl = tf ? static_cast<double>(tv) : pre + static_cast<double>(tv);
+              if (!tf) publish(p, t, ep, 2, incl);
+              misc->lb_prefix[par] = pre;
+              if (t == T - 1 && p.total_out) *p.total_out = incl;
+            }
+          }
+          ptx::named_bar_sync(kEpiBar, kEpiThreads);
+          tprefix = misc->lb_prefix[par];
+        } else if (t == T - 1 && p.total_out && et == 127) {
+          *p.total_out = static_cast<double>(tv);  // last segment lies in this tile
+        }
+        const float cinf =
+            cfl ? cin : static_cast<float>(tprefix + static_cast<double>(cin));
+        // outputs
+        float o[64];
+#pragma unroll
+        for (int j = 0; j < GR; ++j) {
+          const float base = off[j] + (chain[j] ? cinf : 0.f);
+#pragma unroll
+          for (int k = 0; k < G; ++k) {
+            const int e = j * G + k;
+            if (p.exclusive)
+              o[e] = (k == 0) ? (base + 0.f) : (vv[e - 1] + base);
+            else
+              o[e] = vv[e] + base;
+          }
+        }
+        uint8_t* stg = smem + C::OFF_OUT + par * C::OUT_BYTES;
+        const uint32_t rb = static_cast<uint32_t>(rit) * 128u;
+        const uint32_t sw = static_cast<uint32_t>(rit & 7);
+        if constexpr (sizeof(OutT) == 2) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            uint4 w;
+            __half2 h0 = __floats2half2_rn(o[8 * c + 0], o[8 * c + 1]);
+            __half2 h1 = __floats2half2_rn(o[8 * c + 2], o[8 * c + 3]);
+            __half2 h2 = __floats2half2_rn(o[8 * c + 4], o[8 * c + 5]);
+            __half2 h3 = __floats2half2_rn(o[8 * c + 6], o[8 * c + 7]);
+            w.x = *reinterpret_cast<uint32_t*>(&h0);
+            w.y = *reinterpret_cast<uint32_t*>(&h1);
+            w.z = *reinterpret_cast<uint32_t*>(&h2);
+            w.w = *reinterpret_cast<uint32_t*>(&h3);
+            *reinterpret_cast<uint4*>(stg + rb + ((c ^ sw) << 4)) = w;
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              float4 w = make_float4(o[32 * h + 4 * c + 0], o[32 * h + 4 * c + 1],
+                                     o[32 * h + 4 * c + 2], o[32 * h + 4 * c + 3]);
+              *reinterpret_cast<float4*>(stg + h * 16384 + rb + ((c ^ sw) << 4)) = w;
+            }
+          }
+        }
+        if (row == p.rows_full) {  // ragged last row is outside the TMA view: direct stores
+          OutT* out = reinterpret_cast<OutT*>(p.out);
+          for (int k = 0; k < 64; ++k) {
+            const long long e = row * kRow + k;
+            if (e < p.n) out[e] = cvt_out<OutT>(o[k]);
+          }
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(kEpiBar, kEpiThreads);
+        if (leader) {
+          const int32_t r0 = static_cast<int32_t>(t * kTileRows);
+          if constexpr (sizeof(OutT) == 2) {
+            ptx::tma_store_2d(&tout, stg, 0, r0);
+          } else {
+            ptx::tma_store_2d(&tout, stg, 0, r0);
+            ptx::tma_store_2d(&tout, stg + 16384, 32, r0);
+          }
+          ptx::bulk_commit();
+        }
+      }
+    }  // tile loop
+
+    if constexpr (OP == OP_SCAN) {
+      if (leader) ptx::bulk_wait<0>();
+    }
+    // ---- cross-CTA completion: reduce partial fixup / epoch bump
+    const bool need_ticket = (OP == OP_REDUCE) ? (p.need_fixup != 0) : (p.need_lookback != 0);
+    if (need_ticket) {
+      ptx::named_bar_sync(kEpiBar, kEpiThreads);
+      if (leader) {
+        if constexpr (OP == OP_REDUCE) {
+          // open segment at the end of the range -> tail partial
+          const long long lg_end = t_end * (long long)kTileRows * GR;  // one past range's last granule
+          const long long lg = (lg_end < p.qlast + 1 ? lg_end : p.qlast + 1) - 1;
+          const bool closed = ((lg + 1) % p.m == 0) || (lg == p.qlast);
+          Entry e0{misc->head_seg, misc->head_val};
+          Entry e1{closed ? -1LL : lg / p.m, tile_carry};
+          p.entries[2 * cta] = e0;
+          p.entries[2 * cta + 1] = e1;
+        }
+        __threadfence();
+        const unsigned tk = atomicAdd(&p.hdr->ticket, 1u);
+        misc->is_last = (tk == static_cast<unsigned>(Gc - 1));
+      }
+      ptx::named_bar_sync(kEpiBar, kEpiThreads);
+      if (misc->is_last) {
+        __threadfence();
+        if constexpr (OP == OP_REDUCE) {
+          // deterministic combine of partials in CTA order (the paper's grid
+          // pass 2, reduce.py:365-369, done by the last CTA instead of a
+          // second launch).  Stage entries through the now idle input ring.
+          Entry* se = reinterpret_cast<Entry*>(smem);
+          const int ne = 2 * Gc;
+          for (int k = et; k < ne; k += kEpiThreads) {
+            Entry e;
+            e.seg = __ldcg(&p.entries[k].seg);
+            e.val = __ldcg(&p.entries[k].val);
+            se[k] = e;
+          }
+          ptx::named_bar_sync(kEpiBar, kEpiThreads);
+          // each run of equal segment ids is summed by the thread owning its first entry
+          OutT* out = reinterpret_cast<OutT*>(p.out);
+          for (int k = et; k < ne; k += kEpiThreads) {
+            const long long sg = se[k].seg;
+            if (sg < 0) continue;
+            int pk = k - 1;
+            while (pk >= 0 && se[pk].seg < 0) --pk;
+            if (pk >= 0 && se[pk].seg == sg) continue;  // not the first entry of its run
+            double acc = 0.0;
+            for (int kk = k; kk < ne; ++kk) {
+              const long long s2 = se[kk].seg;
+              if (s2 < 0) continue;
+              if (s2 != sg) break;
+              acc += se[kk].val;
+            }
+            out[sg] = cvt_out_d<OutT>(acc);
+          }
+        }
+        if (leader) {
+          p.hdr->epoch = ep;
+          p.hdr->ticket = 0u;
+          __threadfence();
+        }
+      }
+    }
+  }
+
+  // ---- teardown
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// =====================================================================
+// host side
+// =====================================================================
+
+static thread_local char g_err[512] = "";
+static thread_local uint64_t g_launches = 0;
+
+static void set_err(const char* fmt, const char* a = "", long long b = 0) {
+  snprintf(g_err, sizeof(g_err), fmt, a, b);
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+struct DevInfo {
+  int sms = 0;
+  int major = 0;
+  bool ok = false;
+};
+static DevInfo dev_info(int dev) {
+  static DevInfo cache[64];
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= 64) return DevInfo{};
+  if (!cache[dev].ok) {
+    int sms = 0, major = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess)
+      return DevInfo{};
+    cache[dev].sms = sms;
+    cache[dev].major = major;
+    cache[dev].ok = true;
+  }
+  return cache[dev];
+}
+
+static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base,
+                     long long rows, int box_cols) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(kRow), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(kRow) * esize};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(kTileRows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static long long gcd_ll(long long a, long long b) {
+  while (b) {
+    long long t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+static size_t ws_need(int op, long long n, long long seg) {
+  (void)seg;
+  size_t b = kWsLookback;
+  if (op == TC_OP_SCAN) {
+    const long long T = (n + kTileElems - 1) / kTileElems;
+    b += static_cast<size_t>(T) * (sizeof(uint32_t) + 2 * sizeof(double)) + 64;
+  }
+  return (b + 255) & ~size_t(255);
+}
+
+template <int OP, int GR, typename OutT>
+static int launch(const Params& p0, int out_esize, cudaStream_t st) {
+  using C = Cfg<OP, GR, OutT>;
+  constexpr uint32_t smem = smem_bytes<OP, GR, OutT>();
+  auto kern = seg_kernel<OP, GR, OutT>;
+  static std::atomic<int> attr_done{0};
+  if (!attr_done.load()) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess) {
+      set_err("cudaFuncSetAttribute failed: %s", cudaGetErrorString(cudaGetLastError()));
+      return TC_CUDA_ERROR;
+    }
+    attr_done.store(1);
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevInfo di = dev_info(dev);
+  if (!di.ok || di.major < 10) {
+    set_err("no sm_100 device (compute capability major %s%lld)", "", di.major);
+    return TC_NO_DEVICE;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) !=
+          cudaSuccess ||
+      per_sm < 1) {
+    set_err("occupancy query failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return TC_CUDA_ERROR;
+  }
+  long long grid = static_cast<long long>(di.sms) * per_sm;
+  if (grid > p0.num_tiles) grid = p0.num_tiles;
+  if (grid > kMaxCtas) grid = kMaxCtas;
+  if (grid < 1) grid = 1;
+
+  Params p = p0;
+  // tensor maps
+  CUtensorMap tin, tout;
+  const char* wsb = reinterpret_cast<const char*>(p.hdr);
+  const void* in_base = p.rows_full > 0 ? static_cast<const void*>(p.x)
+                                        : static_cast<const void*>(wsb + kWsZeroRow);
+  if (!make_map(&tin, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, in_base,
+                p.rows_full > 0 ? p.rows_full : 1, kRow)) {
+    set_err("cuTensorMapEncodeTiled (input) failed%s%lld", "", 0);
+    return TC_CUDA_ERROR;
+  }
+  if (OP == OP_SCAN) {
+    const void* ob = p.rows_full > 0 ? p.out : static_cast<const void*>(wsb + kWsDummyOut);
+    const bool ok = (out_esize == 2)
+                        ? make_map(&tout, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, ob,
+                                   p.rows_full > 0 ? p.rows_full : 1, kRow)
+                        : make_map(&tout, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ob,
+                                   p.rows_full > 0 ? p.rows_full : 1, 32);
+    if (!ok) {
+      set_err("cuTensorMapEncodeTiled (output) failed%s%lld", "", 0);
+      return TC_CUDA_ERROR;
+    }
+  } else {
+    tout = tin;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  int na = 0;
+  if (OP == OP_SCAN && p.need_lookback) {
+    // decoupled look-back needs every CTA resident: cooperative launch
+    // guarantees co-residency (or fails loudly instead of deadlocking).
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    na = 1;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tin, tout, p);
+  if (e != cudaSuccess) {
+    set_err("kernel launch failed: %s%lld", cudaGetErrorString(e), 0);
+    return TC_CUDA_ERROR;
+  }
+  ++g_launches;
+  return TC_OK;
+}
+
+using LaunchFn = int (*)(const Params&, int, cudaStream_t);
+
+template <int OP, typename OutT>
+static LaunchFn pick(int gr) {
+  switch (gr) {
+    case 1: return &launch<OP, 1, OutT>;
+    case 2: return &launch<OP, 2, OutT>;
+    case 4: return &launch<OP, 4, OutT>;
+    case 8: return &launch<OP, 8, OutT>;
+    case 16: return &launch<OP, 16, OutT>;
+    case 32: return &launch<OP, 32, OutT>;
+    case 64: return &launch<OP, 64, OutT>;
+  }
+  return nullptr;
+}
+
+static int common_checks(const void* x, long long n, long long seg, const void* out, int out_dtype,
+                         bool scan, void* ws, size_t ws_bytes, int op) {
+  if (n < 1 || n >= (1LL << 37)) {
+    set_err("input length %s%lld outside [1, 2^37)", "", n);
+    return TC_BAD_LENGTH;
+  }
+  if (seg < 1) {
+    set_err("segment size must be positive, got %s%lld", "", seg);
+    return TC_BAD_LENGTH;
+  }
+  if (!x || !out || !ws) {
+    set_err("null pointer argument%s%lld", "", 0);
+    return TC_BAD_CONFIG;
+  }
+  if (out_dtype != TC_F16 && out_dtype != TC_F32 && !(out_dtype == TC_F64 && !scan)) {
+    set_err("unsupported output dtype %s%lld", "", out_dtype);
+    return TC_BAD_CONFIG;
+  }
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(out) & 15) ||
+      (reinterpret_cast<uintptr_t>(ws) & 255)) {
+    set_err("x/out must be 16-byte aligned and ws 256-byte aligned%s%lld", "", 0);
+    return TC_BAD_ALIGNMENT;
+  }
+  if (ws_bytes < ws_need(op, n, seg)) {
+    set_err("workspace too small: need %s%lld bytes", "", (long long)ws_need(op, n, seg));
+    return TC_WORKSPACE_TOO_SMALL;
+  }
+  return TC_OK;
+}
+
+static Params make_params(const void* x, long long n, long long seg, void* out, void* ws,
+                          int* gr_out) {
+  if (seg > n) seg = n;  // one segment spanning everything: same result, smaller m
+  Params p{};
+  const long long g = gcd_ll(seg, kRow);
+  const int gr = static_cast<int>(kRow / g);
+  *gr_out = gr;
+  p.x = reinterpret_cast<const __half*>(x);
+  p.out = out;
+  p.n = n;
+  p.seg = seg;
+  p.m = seg / g;
+  p.rows_full = n / kRow;
+  p.num_tiles = (n + kTileElems - 1) / kTileElems;
+  p.qlast = (n - 1) / g;
+  char* w = reinterpret_cast<char*>(ws);
+  p.hdr = reinterpret_cast<WsHeader*>(w);
+  p.entries = reinterpret_cast<Entry*>(w + kWsEntries);
+  const long long T = p.num_tiles;
+  p.lb_flag = reinterpret_cast<uint32_t*>(w + kWsLookback);
+  size_t off = kWsLookback + ((static_cast<size_t>(T) * 4 + 15) & ~size_t(15));
+  p.lb_agg = reinterpret_cast<double*>(w + off);
+  off += static_cast<size_t>(T) * 8;
+  p.lb_inc = reinterpret_cast<double*>(w + off);
+  p.need_fixup = (kTileElems % seg != 0) ? 1 : 0;
+  return p;
+}
+
+}  // namespace tc
+
+// =====================================================================
+// C ABI
+// =====================================================================
+using namespace tc;
+
+extern "C" {
+
+size_t tc_workspace_bytes(int op, int64_t n, int64_t seg) {
+  if (n < 1) n = 1;
+  return ws_need(op, n, seg);
+}
+
+int tc_seg_reduce(const void* x, int64_t n, int64_t seg, void* out, int out_dtype, void* ws,
+                  size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  int rc = common_checks(x, n, seg, out, out_dtype, false, ws, ws_bytes, TC_OP_REDUCE);
+  if (rc) return rc;
+  int gr = 0;
+  Params p = make_params(x, n, seg, out, ws, &gr);
+  LaunchFn fn = nullptr;
+  int es = 2;
+  if (out_dtype == TC_F16) {
+    fn = pick<OP_REDUCE, __half>(gr);
+    es = 2;
+  } else if (out_dtype == TC_F32) {
+    fn = pick<OP_REDUCE, float>(gr);
+    es = 4;
+  } else {
+    fn = pick<OP_REDUCE, double>(gr);
+    es = 8;
+  }
+  if (!fn) {
+    set_err("no kernel for granules-per-row %s%lld", "", gr);
+    return TC_BAD_CONFIG;
+  }
+  return fn(p, es, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int tc_full_reduce(const void* x, int64_t n, void* out, int out_dtype, void* ws, size_t ws_bytes,
+                   void* stream) {
+  return tc_seg_reduce(x, n, n < 1 ? 1 : n, out, out_dtype, ws, ws_bytes, stream);
+}
+
+int tc_seg_scan(const void* x, int64_t n, int64_t seg, void* out, int out_dtype, int exclusive,
+                const double* carry_in, double* total_out, void* ws, size_t ws_bytes,
+                void* stream) {
+  g_err[0] = 0;
+  int rc = common_checks(x, n, seg, out, out_dtype, true, ws, ws_bytes, TC_OP_SCAN);
+  if (rc) return rc;
+  int gr = 0;
+  Params p = make_params(x, n, seg, out, ws, &gr);
+  p.exclusive = exclusive ? 1 : 0;
+  p.carry_in = carry_in;
+  p.total_out = total_out;
+  p.need_lookback = ((kTileElems % p.seg) != 0 || carry_in != nullptr) ? 1 : 0;
+  LaunchFn fn = (out_dtype == TC_F16) ? pick<OP_SCAN, __half>(gr) : pick<OP_SCAN, float>(gr);
+  if (!fn) {
+    set_err("no kernel for granules-per-row %s%lld", "", gr);
+    return TC_BAD_CONFIG;
+  }
+  return fn(p, out_dtype == TC_F16 ? 2 : 4, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int tc_full_scan(const void* x, int64_t n, void* out, int out_dtype, int exclusive,
+                 const double* carry_in, double* total_out, void* ws, size_t ws_bytes,
+                 void* stream) {
+  return tc_seg_scan(x, n, n < 1 ? 1 : n, out, out_dtype, exclusive, carry_in, total_out, ws,
+                     ws_bytes, stream);
+}
+
+const char* tc_status_string(int s) {
+  switch (s) {
+    case TC_OK: return "ok";
+    case TC_BAD_LENGTH: return "bad length";
+    case TC_BAD_CONFIG: return "bad config";
+    case TC_BAD_ALIGNMENT: return "bad alignment";
+    case TC_WORKSPACE_TOO_SMALL: return "workspace too small";
+    case TC_CUDA_ERROR: return "cuda error";
+    case TC_NO_DEVICE: return "no sm_100 device";
+  }
+  return "unknown status";
+}
+
+const char* tc_last_error(void) { return g_err; }
+
+uint64_t tc_launch_count(void) { return g_launches; }
+void tc_reset_launch_count(void) { g_launches = 0; }
+
+int tc_abi_version(void) { return (1 << 16) | 0; }
+
+}  // extern "C"
