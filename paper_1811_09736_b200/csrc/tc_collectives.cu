@@ -1,7 +1,7 @@
 // tc_collectives.cu -- B200 (sm_100a) tensor-core segmented reduction and
 // scan (arXiv 1811.09736), behind the C ABI in include/tc_collectives.h.
 //
-// Design (see DESIGN.md for the full story):
+// Design (DESIGN.md has the full story):
 //
 //  * Data view.  The fp16 input is a row-major matrix X[R x 64] (one row =
 //    128 B = one SW128 swizzle atom).  A tile is 128 consecutive rows
@@ -18,19 +18,25 @@
 //                triangular ones with g x g blocks) -> in-granule inclusive
 //                prefix sums of every row            (the A.U step)
 //    with fp16 operands from SMEM descriptors and fp32 accumulators in TMEM.
-//    The P-side / L-side combine (across granules, rows, tiles, CTAs) is
-//    the carry chain: a segmented (value, flag) scan in registers, warp
-//    shuffles across the 32 rows of a warp, shared memory across the four
-//    epilogue warps, registers across a CTA's tiles (reduce) and a
-//    decoupled look-back over tiles (scan), all in fp32/fp64.
+//    The P-side / L-side combine across granules, rows, tiles and CTAs is
+//    the carry chain, specialised by how segments align with the tiling:
+//        MODE_LOCAL    seg == g (divides 64): no carries at all
+//        MODE_ROWS     seg = 64*2^k <= 8192: aligned row groups (shuffles)
+//        MODE_TILES    seg = 8192*k: whole tiles, CTA-sequential fp64 carry
+//        MODE_GENERAL  anything else: segmented (value, flag) pair scan
+//        MODE_LOOKBACK scan of huge segments: round-robin tiles + decoupled
+//                      look-back (fp64 aggregates / prefixes in HBM)
+//    Reductions and bounded-segment scans give every CTA one contiguous
+//    tile range; a reduce combines the segments cut by range boundaries in
+//    a deterministic last-CTA fixup, a scan recomputes the carry entering
+//    its range from the (< seg) preceding elements.
 //
-//  * Warp specialisation (192 threads, persistent grid): warp 0 = TMA
-//    producer, warp 1 = TMEM allocator + single-thread MMA issuer, warps
-//    2..5 = epilogue (TMEM lane quadrant = warp % 4).  mbarrier rings:
-//    full/empty (TMA <-> MMA) and tmem_full/tmem_empty (MMA <-> epilogue).
-//
+//  * Warp specialisation (192 threads, persistent grid, 2 CTAs/SM): warp 0
+//    = TMA producer, warp 1 = TMEM allocator + single-thread MMA issuer,
+//    warps 2..5 = epilogue (TMEM lane quadrant = warp % 4).  mbarrier
+//    rings: full/empty (TMA <-> MMA), tmem_full/tmem_empty (MMA <-> epi).
 //  * Scan outputs are staged through swizzled shared memory and written by
-//    TMA stores; reduce outputs are written with plain coalesced stores.
+//    TMA bulk-tensor stores; reduce outputs use plain coalesced stores.
 //
 // Reference correspondence (pkg/src/halftile):
 //    reduce granule sums     reduce.py:92-106 (Reduction16 P.A), :171-198
@@ -55,16 +61,22 @@
 
 namespace tc {
 
-constexpr int kRow = 64;                              // elements per row
-constexpr int kTileRows = 128;                        // UMMA M
-constexpr int kTileElems = kRow * kTileRows;          // 8192
-constexpr uint32_t kTileBytes = kTileElems * 2;       // 16 KB of fp16
-constexpr int kThreads = 192;                         // 6 warps
-constexpr int kEpiThreads = 128;                      // warps 2..5
-constexpr int kEpiBar = 1;                            // named barrier id
+constexpr int kRow = 64;                         // elements per row
+constexpr int kTileRows = 128;                   // UMMA M
+constexpr int kTileElems = kRow * kTileRows;     // 8192
+constexpr uint32_t kTileBytes = kTileElems * 2;  // 16 KB of fp16
+constexpr int kThreads = 192;                    // 6 warps
+constexpr int kEpiThreads = 128;                 // warps 2..5
+constexpr int kEpiBar = 1;                       // named barrier id
 constexpr int OP_REDUCE = 0;
 constexpr int OP_SCAN = 1;
-constexpr int kMaxCtas = 1024;                        // persistent grid cap
+constexpr int MODE_LOCAL = 0;
+constexpr int MODE_ROWS = 1;
+constexpr int MODE_TILES = 2;
+constexpr int MODE_GENERAL = 3;
+constexpr int MODE_LOOKBACK = 4;
+constexpr int kMaxCtas = 1024;                    // persistent grid cap
+constexpr long long kScanPrepassMax = 1LL << 18;  // largest seg whose range-entry carry is recomputed
 constexpr unsigned kFull = 0xffffffffu;
 
 struct WsHeader {
@@ -91,6 +103,11 @@ struct Params {
   long long rows_full;  // n / 64
   long long num_tiles;  // ceil(n / 8192)
   long long qlast;      // index of the last granule, (n - 1) / g
+  long long nseg;       // ceil(n / seg)
+  long long step_div;   // GENERAL: (128 * GR) / m   (granule step per tile)
+  long long step_mod;   // GENERAL: (128 * GR) % m
+  long long ktiles;     // TILES: tiles per segment
+  int log2m;            // ROWS: log2(rows per segment)
   const double* carry_in;
   double* total_out;
   WsHeader* hdr;
@@ -99,8 +116,7 @@ struct Params {
   double* lb_agg;
   double* lb_inc;
   int exclusive;
-  int need_fixup;     // reduce: segments may straddle CTA ranges
-  int need_lookback;  // scan: segments may straddle tiles (or carry_in given)
+  int need_fixup;  // reduce: segments may straddle CTA ranges
 };
 
 template <typename T>
@@ -137,19 +153,21 @@ __host__ __device__ constexpr int pow2_at_least(int v) {
   return v <= 32 ? 32 : v <= 64 ? 64 : v <= 128 ? 128 : v <= 256 ? 256 : 512;
 }
 
-template <int OP, int GR, typename OutT>
+template <int OP, int GR, int MODE, typename OutT>
 struct Cfg {
-  static constexpr int G = 64 / GR;  // granule size (elements)
+  static constexpr int G = 64 / GR;                                      // granule size
   static constexpr int N = (OP == OP_SCAN) ? 64 : (GR < 16 ? 16 : GR);  // UMMA N
-  static constexpr int STAGES = (OP == OP_SCAN && sizeof(OutT) == 4) ? 6 : 8;
+  static constexpr int MINB = (OP == OP_SCAN && GR >= 32) ? 1 : 2;      // CTAs per SM
+  static constexpr int STAGES = (OP == OP_REDUCE) ? (MINB == 2 ? 6 : 8) : (MINB == 2 ? 4 : 6);
   static constexpr int ACC = 4;  // TMEM accumulator stages
   static constexpr int TMEM_COLS = pow2_at_least(ACC * N);
-  static constexpr int OUT_BUFS = (OP == OP_SCAN) ? 2 : 0;
+  static constexpr int OUT_BUFS = (OP == OP_SCAN) ? ((sizeof(OutT) == 4 && MINB == 2) ? 1 : 2) : 0;
   static constexpr uint32_t OUT_BYTES = kTileElems * sizeof(OutT);
   static constexpr uint32_t OFF_B = STAGES * kTileBytes;
   static constexpr uint32_t OFF_OUT = OFF_B + ((N * 128 + 1023) / 1024) * 1024;
   static constexpr uint32_t OFF_MISC = OFF_OUT + OUT_BUFS * OUT_BYTES;
   static constexpr int LD_COLS = (OP == OP_SCAN) ? 64 : GR;  // TMEM columns read per tile
+  static constexpr bool CONTIG = (MODE != MODE_LOOKBACK);    // contiguous CTA tile ranges
 };
 
 template <int STAGES, int ACC>
@@ -162,14 +180,15 @@ struct Misc {
   int is_last;
   float pv[2][4];
   int pf[2][4];
+  double dsum[4];
   double lb_prefix[2];
   long long head_seg;
   double head_val;
 };
 
-template <int OP, int GR, typename OutT>
+template <int OP, int GR, int MODE, typename OutT>
 constexpr uint32_t smem_bytes() {
-  using C = Cfg<OP, GR, OutT>;
+  using C = Cfg<OP, GR, MODE, OutT>;
   return C::OFF_MISC + sizeof(Misc<C::STAGES, C::ACC>) + 1024;  // +1024: alignment slack
 }
 
@@ -215,6 +234,62 @@ __device__ __forceinline__ void warp_pair_scan(float& v, int& f, int lane) {
   }
 }
 
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float warp_incl_scan(float v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const float u = __shfl_up_sync(kFull, v, d);
+    if (lane >= d) v += u;
+  }
+  return v;
+}
+
+// Sum of x[lo, hi) in fp64 by the 128 epilogue threads (all get the result).
+template <typename MiscT>
+__device__ double epi_range_sum(const __half* x, long long lo, long long hi, int et, int lane,
+                                int qd, MiscT* misc) {
+  double acc = 0.0;
+  if (hi > lo) {
+    long long a = (lo + 7) & ~7LL;  // 16-B aligned start
+    if (a > hi) a = hi;
+    if (et == 0)
+      for (long long e = lo; e < a; ++e) acc += __half2float(x[e]);
+    const long long nb = (hi - a) >> 3;  // whole 8-element blocks
+    const uint4* xv = reinterpret_cast<const uint4*>(x + a);
+    float fs = 0.f;
+    int cnt = 0;
+    for (long long b = et; b < nb; b += kEpiThreads) {
+      const uint4 w = __ldg(xv + b);
+      const __half2* h = reinterpret_cast<const __half2*>(&w);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f2 = __half22float2(h[k]);
+        fs += f2.x + f2.y;
+      }
+      if (++cnt == 64) {  // flush to fp64 every 512 elements
+        acc += fs;
+        fs = 0.f;
+        cnt = 0;
+      }
+    }
+    acc += fs;
+    if (et == kEpiThreads - 1)
+      for (long long e = a + nb * 8; e < hi; ++e) acc += __half2float(x[e]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+  if (lane == 0) misc->dsum[qd] = acc;
+  ptx::named_bar_sync(kEpiBar, kEpiThreads);
+  const double r = misc->dsum[0] + misc->dsum[1] + misc->dsum[2] + misc->dsum[3];
+  ptx::named_bar_sync(kEpiBar, kEpiThreads);
+  return r;
+}
+
 // Decoupled look-back over tiles: exclusive running value entering tile t.
 // Lane i inspects tile (t-1-i) - 32*w.  Status word = (epoch << 2) | state,
 // state 1 = aggregate published (lb_agg), 2 = inclusive published (lb_inc).
@@ -254,31 +329,61 @@ __device__ __forceinline__ void publish(const Params& p, long long t, uint32_t e
   ptx::st_release_u32(p.lb_flag + t, (ep << 2) | static_cast<uint32_t>(state));
 }
 
-template <int OP, int GR, typename OutT>
-__global__ void __launch_bounds__(kThreads, 1)
+// Store GR consecutive outputs out[q0 .. q0+GR) (vectorised when aligned).
+template <typename OutT, int GR>
+__device__ __forceinline__ void store_run(OutT* out, long long q0, const float (&v)[GR],
+                                          long long qlast) {
+  if (q0 + GR - 1 <= qlast) {
+    if constexpr (sizeof(OutT) == 4 && GR % 4 == 0) {
+#pragma unroll
+      for (int j = 0; j < GR; j += 4)
+        *reinterpret_cast<float4*>(out + q0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      return;
+    } else if constexpr (sizeof(OutT) == 2 && GR % 4 == 0) {
+#pragma unroll
+      for (int j = 0; j < GR; j += 4) {
+        __half2 a = __floats2half2_rn(v[j], v[j + 1]);
+        __half2 b = __floats2half2_rn(v[j + 2], v[j + 3]);
+        uint2 w;
+        w.x = *reinterpret_cast<uint32_t*>(&a);
+        w.y = *reinterpret_cast<uint32_t*>(&b);
+        *reinterpret_cast<uint2*>(out + q0 + j) = w;
+      }
+      return;
+    } else if constexpr (sizeof(OutT) == 4 && GR == 2) {
+      *reinterpret_cast<float2*>(out + q0) = make_float2(v[0], v[1]);
+      return;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < GR; ++j)
+    if (q0 + j <= qlast) out[q0 + j] = cvt_out<OutT>(v[j]);
+}
+
+template <int OP, int GR, int MODE, typename OutT>
+__global__ void __launch_bounds__(kThreads, (Cfg<OP, GR, MODE, OutT>::MINB))
     seg_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
                const Params p) {
-  using C = Cfg<OP, GR, OutT>;
+  using C = Cfg<OP, GR, MODE, OutT>;
   using MiscT = Misc<C::STAGES, C::ACC>;
   constexpr int G = C::G;
   constexpr int N = C::N;
   constexpr int STAGES = C::STAGES;
   constexpr int ACC = C::ACC;
 
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem =
-      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   MiscT* misc = reinterpret_cast<MiscT*>(smem + C::OFF_MISC);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  // ---- work assignment: reduce = contiguous tile range, scan = round robin
+  // ---- work assignment: contiguous tile range (round robin for LOOKBACK)
   const long long T = p.num_tiles;
   const int Gc = gridDim.x;
   const int cta = blockIdx.x;
   long long t_begin, t_end;
   int t_count;
-  if (OP == OP_REDUCE) {
+  if constexpr (C::CONTIG) {
     t_begin = T * cta / Gc;
     t_end = T * (cta + 1) / Gc;
     t_count = static_cast<int>(t_end - t_begin);
@@ -288,9 +393,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     t_count = static_cast<int>((T - cta + Gc - 1) / Gc);
   }
   auto tile_of = [&](int i) -> long long {
-    return OP == OP_REDUCE ? t_begin + i : static_cast<long long>(cta) + static_cast<long long>(i) * Gc;
+    if constexpr (C::CONTIG)
+      return t_begin + i;
+    else
+      return static_cast<long long>(cta) + static_cast<long long>(i) * Gc;
   };
-  const uint32_t ep = (p.hdr->epoch + 1u) & 0x3FFFFFFFu;
 
   // ---- one-time setup
   if (warp == 0 && lane == 0) {
@@ -356,21 +463,45 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     // ================= epilogue (warps 2..5) =================
-    const int qd = warp & 3;                 // TMEM lane quadrant
-    const int rit = qd * 32 + lane;          // row in tile
-    const int et = threadIdx.x - 64;         // epilogue thread id 0..127
+    const int qd = warp & 3;          // TMEM lane quadrant
+    const int rit = qd * 32 + lane;   // row in tile
+    const int et = threadIdx.x - 64;  // epilogue thread id 0..127
     const bool leader = (et == 0);
     const uint32_t lane_base = static_cast<uint32_t>(qd * 32) << 16;
-    const long long range_first_elem = t_begin * kTileElems;  // reduce only
-    double tile_carry = 0.0;  // reduce: open segment value entering the tile (CTA-local)
+    const long long range_first_elem = t_begin * kTileElems;
     const bool has_carry = (p.carry_in != nullptr);
-    const double carry0 = (OP == OP_SCAN && has_carry) ? *p.carry_in : 0.0;
+    const uint32_t ep = (p.hdr->epoch + 1u) & 0x3FFFFFFFu;
+
+    // running state
+    double carry = 0.0;  // value of the segment open at the current tile's entry
+    long long q0 = (tile_of(0) * kTileRows + rit) * GR;  // first granule of this row
+    long long qmod = 0, qdiv = 0;                        // GENERAL: q0 % m, q0 / m
+    long long tpos = 0, tseg = 0;                        // TILES: t % k, t / k
+    if constexpr (MODE == MODE_GENERAL) {
+      qmod = q0 % p.m;
+      qdiv = q0 / p.m;
+    }
+    if constexpr (MODE == MODE_TILES) {
+      tpos = t_begin % p.ktiles;
+      tseg = t_begin / p.ktiles;
+    }
+    if constexpr (OP == OP_SCAN && (MODE == MODE_TILES || MODE == MODE_GENERAL)) {
+      // carry entering this CTA's range: the (< seg) elements of the open
+      // segment that precede the range, re-read from HBM (bounded by
+      // kScanPrepassMax), plus the caller's carry for segment 0.
+      const long long seg_start = (range_first_elem / p.seg) * p.seg;
+      carry = epi_range_sum(p.x, seg_start, range_first_elem, et, lane, qd, misc);
+      if (seg_start == 0 && has_carry) carry += *p.carry_in;
+    }
 
     for (int i = 0; i < t_count; ++i) {
       const long long t = tile_of(i);
       const int a = i % ACC;
       const uint32_t aph = (i / ACC) & 1;
       const int par = i & 1;
+      if constexpr (!C::CONTIG) {
+        q0 = (t * kTileRows + rit) * GR;
+      }
       ptx::mbar_wait(&misc->tfull[a], aph);
       ptx::tc_fence_after();
       constexpr int LD = C::LD_COLS;
@@ -388,16 +519,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_arrive(&misc->tempty[a]);
 
       const long long row = t * kTileRows + rit;
-      const long long q0 = row * GR;  // first granule of this row
 
       if constexpr (OP == OP_REDUCE) {
-        // ---------------------------------------------------------- reduce
+        // ================================================= reduce
         float gs[GR];
 #pragma unroll
         for (int j = 0; j < GR; ++j) gs[j] = __uint_as_float(r[j]);
         if (row == p.rows_full) {  // ragged last row: beyond the TMA view, patch from HBM
           const long long e0 = row * kRow;
-#pragma unroll 1
+#pragma unroll
           for (int j = 0; j < GR; ++j) {
             float s = 0.f;
             for (int k = 0; k < G; ++k) {
@@ -408,129 +538,78 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         OutT* out = reinterpret_cast<OutT*>(p.out);
-        if (p.m == 1) {
-          // every granule is a whole segment: out[q0 + j] = gs[j]
-          if (q0 + GR - 1 <= p.qlast) {
-#pragma unroll
-            for (int j = 0; j < GR; ++j) out[q0 + j] = cvt_out<OutT>(gs[j]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < GR; ++j)
-              if (q0 + j <= p.qlast) out[q0 + j] = cvt_out<OutT>(gs[j]);
-          }
-          continue;
-        }
-        // thread-local pass over the row's granules.  `seg` always indexes
-        // the segment containing granule q0 + j.
-        long long rem = p.m - 1 - (q0 % p.m);  // granules until the next segment end
-        long long seg = (q0 + rem) / p.m;
-        const long long seg0 = seg;            // segment closed by the row's first end
-        float run = 0.f, head = 0.f;
-        int seen = 0;
-#pragma unroll
-        for (int j = 0; j < GR; ++j) {
-          run += gs[j];
-          const long long qj = q0 + j;
-          if (qj <= p.qlast && (rem == 0 || qj == p.qlast)) {
-            if (!seen) {
-              head = run;  // needs the carry from earlier rows / tiles
-              seen = 1;
-            } else {
-              out[seg] = cvt_out<OutT>(run);  // segment wholly inside this row
+        if constexpr (MODE == MODE_LOCAL) {
+          store_run<OutT, GR>(out, q0, gs, p.qlast);
+        } else if constexpr (MODE == MODE_ROWS) {
+          // segments = aligned groups of 2^log2m rows inside the tile
+          float v = gs[0];
+          const int msz = 1 << p.log2m;
+          if (msz <= 32) {
+            for (int d = 1; d < msz; d <<= 1) v += __shfl_xor_sync(kFull, v, d);
+            if ((lane & (msz - 1)) == 0) {
+              const long long sg = row >> p.log2m;
+              if (sg < p.nseg) out[sg] = cvt_out<OutT>(v);
             }
-            ++seg;
-            run = 0.f;
-          }
-          rem = (rem == 0) ? p.m - 1 : rem - 1;
-        }
-        // cross-row segmented scan of (tail run, has_end)
-        float v = run;
-        int f = seen;
-        warp_pair_scan(v, f, lane);
-        float ve = __shfl_up_sync(kFull, v, 1);
-        int fe = __shfl_up_sync(kFull, f, 1);
-        if (lane == 0) {
-          ve = 0.f;
-          fe = 0;
-        }
-        if (lane == 31) {
-          misc->pv[par][qd] = v;
-          misc->pf[par][qd] = f;
-        }
-        ptx::named_bar_sync(kEpiBar, kEpiThreads);
-        float wv = 0.f, tv = 0.f;
-        int wf = 0, tf = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float yv = misc->pv[par][k];
-          const int yf = misc->pf[par][k];
-          if (k < qd) compose(wv, wf, yv, yf);
-          compose(tv, tf, yv, yf);
-        }
-        float cin = ve;
-        int cfl = fe;
-        {
-          float xv = wv;
-          int xf = wf;
-          compose(xv, xf, ve, fe);
-          cin = xv;
-          cfl = xf;
-        }
-        if (seen) {
-          const double val = static_cast<double>(cin + head) + (cfl ? 0.0 : tile_carry);
-          if (seg0 * p.seg < range_first_elem) {
-            misc->head_seg = seg0;  // partial: segment began in an earlier CTA's range
-            misc->head_val = val;
           } else {
-            out[seg0] = cvt_out_d<OutT>(val);
+            v = warp_sum(v);
+            if (lane == 0) misc->pv[par][qd] = v;
+            ptx::named_bar_sync(kEpiBar, kEpiThreads);
+            if (lane == 0) {
+              if (msz == 64 && (qd & 1) == 0) {
+                const long long sg = row >> 6;
+                if (sg < p.nseg)
+                  out[sg] = cvt_out<OutT>(misc->pv[par][qd] + misc->pv[par][qd + 1]);
+              } else if (msz == 128 && qd == 0) {
+                const float s4 = (misc->pv[par][0] + misc->pv[par][1]) +
+                                 (misc->pv[par][2] + misc->pv[par][3]);
+                out[t] = cvt_out<OutT>(s4);
+              }
+            }
           }
-        }
-        tile_carry = tf ? static_cast<double>(tv) : tile_carry + static_cast<double>(tv);
-      } else {
-        // ------------------------------------------------------------ scan
-        float vv[64];
-#pragma unroll
-        for (int k = 0; k < 64; ++k) vv[k] = __uint_as_float(r[k]);
-        if (row == p.rows_full) {  // ragged last row: recompute in-granule scans from HBM
-          const long long e0 = row * kRow;
-          float s = 0.f;
-#pragma unroll
-          for (int k = 0; k < 64; ++k) {
-            if (k % G == 0) s = 0.f;
-            const long long e = e0 + k;
-            s += (e < p.n) ? __half2float(p.x[e]) : 0.f;
-            vv[k] = s;
+        } else if constexpr (MODE == MODE_TILES) {
+          // whole tiles belong to one segment of ktiles tiles
+          const float v = warp_sum(gs[0]);
+          if (lane == 0) misc->pv[par][qd] = v;
+          ptx::named_bar_sync(kEpiBar, kEpiThreads);
+          const float tsum = (misc->pv[par][0] + misc->pv[par][1]) +
+                             (misc->pv[par][2] + misc->pv[par][3]);
+          if (tpos == 0) carry = 0.0;
+          carry += static_cast<double>(tsum);
+          if ((tpos == p.ktiles - 1 || t == T - 1) && leader) {
+            if (tseg * p.seg < range_first_elem) {
+              misc->head_seg = tseg;  // began in an earlier CTA's range
+              misc->head_val = carry;
+            } else {
+              out[tseg] = cvt_out_d<OutT>(carry);
+            }
           }
-        }
-        // thread-local pass: starts, local offsets, chain-to-row-start flags
-        float off[GR];
-        int chain[GR];
-        float run = 0.f;
-        int seen = 0;
-        {
-          long long rem = (p.m - (q0 % p.m)) % p.m;  // granules until the next start
+          if (++tpos == p.ktiles) {
+            tpos = 0;
+            ++tseg;
+          }
+        } else {
+          // MODE_GENERAL: segmented (value, has_end) pair scan over rows
+          long long rem = p.m - 1 - qmod;  // granules until the next segment end
+          long long sg = qdiv;             // segment containing granule q0 + j
+          const long long seg0 = sg;       // segment closed by the row's first end
+          float run = 0.f, head = 0.f;
+          int seen = 0;
 #pragma unroll
           for (int j = 0; j < GR; ++j) {
-            const bool st = (rem == 0) && (q0 + j <= p.qlast) && !((q0 + j) == 0 && has_carry);
-            if (st) {
+            run += gs[j];
+            const long long qj = q0 + j;
+            if (qj <= p.qlast && (rem == 0 || qj == p.qlast)) {
+              if (!seen) {
+                head = run;  // needs the carry from earlier rows / tiles
+                seen = 1;
+              } else {
+                out[sg] = cvt_out<OutT>(run);  // segment wholly inside this row
+              }
+              ++sg;
               run = 0.f;
-              seen = 1;
             }
-            off[j] = run;
-            chain[j] = !seen;
-            run += vv[j * G + G - 1];
             rem = (rem == 0) ? p.m - 1 : rem - 1;
           }
-        }
-        // staging buffer reuse: the TMA store issued two tiles ago must have
-        // finished reading it before anyone writes.
-        if (leader) ptx::bulk_wait_read<1>();
-        float cin = 0.f;
-        int cfl = 1;
-        float tv = 0.f;
-        int tf = 1;
-        const bool need_rows = (p.m != 1) || has_carry || (p.total_out != nullptr);
-        if (need_rows) {
           float v = run;
           int f = seen;
           warp_pair_scan(v, f, lane);
@@ -545,10 +624,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             misc->pf[par][qd] = f;
           }
           ptx::named_bar_sync(kEpiBar, kEpiThreads);
-          float wv = 0.f;
-          int wf = 0;
-          tv = 0.f;
-          tf = 0;
+          float wv = 0.f, tv = 0.f;
+          int wf = 0, tf = 0;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const float yv = misc->pv[par][k];
@@ -557,69 +634,217 @@ __global__ void __launch_bounds__(kThreads, 1)
             compose(tv, tf, yv, yf);
           }
           compose(wv, wf, ve, fe);
-          cin = wv;
-          cfl = wf;
+          if (seen) {
+            const double val = static_cast<double>(wv + head) + (wf ? 0.0 : carry);
+            if (seg0 * p.seg < range_first_elem) {
+              misc->head_seg = seg0;  // partial: segment began in an earlier CTA's range
+              misc->head_val = val;
+            } else {
+              out[seg0] = cvt_out_d<OutT>(val);
+            }
+          }
+          carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
+          // advance to the next tile's row (contiguous ranges)
+          qmod += p.step_mod;
+          qdiv += p.step_div;
+          if (qmod >= p.m) {
+            qmod -= p.m;
+            ++qdiv;
+          }
+        }
+        q0 += static_cast<long long>(kTileRows) * GR;
+      } else {
+        // ================================================= scan
+        float vv[64];
+#pragma unroll
+        for (int k = 0; k < 64; ++k) vv[k] = __uint_as_float(r[k]);
+        if (row == p.rows_full) {  // ragged last row: recompute in-granule scans from HBM
+          const long long e0 = row * kRow;
+          float s = 0.f;
+#pragma unroll
+          for (int k = 0; k < 64; ++k) {
+            if (k % G == 0) s = 0.f;
+            const long long e = e0 + k;
+            s += (e < p.n) ? __half2float(p.x[e]) : 0.f;
+            vv[k] = s;
+          }
+        }
+        // staging buffer reuse: the TMA store that last used this buffer
+        // must have finished reading it before anyone writes (barrier below).
+        if (leader) ptx::bulk_wait_read<C::OUT_BUFS - 1>();
+        float off[GR];  // per-granule offset to add (exclusive prefix within segment)
+        if constexpr (MODE == MODE_LOCAL) {
+          ptx::named_bar_sync(kEpiBar, kEpiThreads);
+#pragma unroll
+          for (int j = 0; j < GR; ++j) off[j] = 0.f;
+        } else if constexpr (MODE == MODE_ROWS) {
+          const float tot = vv[63];
+          const int msz = 1 << p.log2m;
+          float incl = tot;
+          float excl;
+          if (msz <= 32) {
+            const int pos = lane & (msz - 1);
+            for (int d = 1; d < msz; d <<= 1) {
+              const float u = __shfl_up_sync(kFull, incl, d);
+              if (pos >= d) incl += u;
+            }
+            excl = __shfl_up_sync(kFull, incl, 1);
+            if (pos == 0) excl = 0.f;
+            ptx::named_bar_sync(kEpiBar, kEpiThreads);
+          } else {
+            incl = warp_incl_scan(incl, lane);
+            excl = __shfl_up_sync(kFull, incl, 1);
+            if (lane == 0) excl = 0.f;
+            if (lane == 31) misc->pv[par][qd] = incl;
+            ptx::named_bar_sync(kEpiBar, kEpiThreads);
+            float woff = 0.f;
+            if (msz == 64) {
+              if (qd & 1) woff = misc->pv[par][qd - 1];
+            } else {
+#pragma unroll
+              for (int k = 0; k < 3; ++k)
+                if (k < qd) woff += misc->pv[par][k];
+            }
+            excl += woff;
+          }
+          off[0] = excl;
+        } else if constexpr (MODE == MODE_TILES) {
+          const float tot = vv[63];
+          float incl = warp_incl_scan(tot, lane);
+          float excl = __shfl_up_sync(kFull, incl, 1);
+          if (lane == 0) excl = 0.f;
+          if (lane == 31) misc->pv[par][qd] = incl;
+          ptx::named_bar_sync(kEpiBar, kEpiThreads);
+          float woff = 0.f, ttot = 0.f;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float y = misc->pv[par][k];
+            if (k < qd) woff += y;
+            ttot += y;
+          }
+          if (tpos == 0) carry = 0.0;  // a segment starts at this tile
+          off[0] = static_cast<float>(carry + static_cast<double>(excl + woff));
+          carry += static_cast<double>(ttot);
+          if (++tpos == p.ktiles) {
+            tpos = 0;
+            ++tseg;
+          }
         } else {
-          ptx::named_bar_sync(kEpiBar, kEpiThreads);
-        }
-        // tile prefix (look-back) for segments entering this tile
-        double tprefix = 0.0;
-        if (p.need_lookback) {
-          const long long tq0 = t * (long long)kTileRows * GR;  // first granule of the tile
-          const bool first_start = (tq0 % p.m == 0) && !(t == 0 && has_carry);
-          if (warp == 2) {
-            if (lane == 0) {
-              if (tf)
-                publish(p, t, ep, 2, static_cast<double>(tv));
-              else if (!(t == 0 || first_start))
-                publish(p, t, ep, 1, static_cast<double>(tv));
-            }
-            double pre;
-            if (t == 0)
-              pre = carry0;
-            else if (first_start)
-              pre = 0.0;
-            else
-              pre = lookback(p, t, ep, lane);
-            if (lane == 0) {
-              const double incl = tf ? static_cast<double>(tv) : pre + static_cast<double>(tv);
-              if (!tf) publish(p, t, ep, 2, incl);
-              misc->lb_prefix[par] = pre;
-              if (t == T - 1 && p.total_out) *p.total_out = incl;
+          // MODE_GENERAL / MODE_LOOKBACK: pair scan with granule starts
+          int chain[GR];
+          float run = 0.f;
+          int seen = 0;
+          {
+            long long qm = (MODE == MODE_GENERAL) ? qmod : (q0 % p.m);
+            long long rem = qm == 0 ? 0 : p.m - qm;  // granules until the next start
+#pragma unroll
+            for (int j = 0; j < GR; ++j) {
+              const bool st =
+                  (rem == 0) && (q0 + j <= p.qlast) && !((q0 + j) == 0 && has_carry);
+              if (st) {
+                run = 0.f;
+                seen = 1;
+              }
+              off[j] = run;
+              chain[j] = !seen;
+              run += vv[j * G + G - 1];
+              rem = (rem == 0) ? p.m - 1 : rem - 1;
             }
           }
-          ptx::named_bar_sync(kEpiBar, kEpiThreads);
-          tprefix = misc->lb_prefix[par];
-        } else if (t == T - 1 && p.total_out && et == 127) {
-          *p.total_out = static_cast<double>(tv);  // last segment lies in this tile
-        }
-        const float cinf =
-            cfl ? cin : static_cast<float>(tprefix + static_cast<double>(cin));
-        // outputs
-        float o[64];
-#pragma unroll
-        for (int j = 0; j < GR; ++j) {
-          const float base = off[j] + (chain[j] ? cinf : 0.f);
-#pragma unroll
-          for (int k = 0; k < G; ++k) {
-            const int e = j * G + k;
-            if (p.exclusive)
-              o[e] = (k == 0) ? (base + 0.f) : (vv[e - 1] + base);
-            else
-              o[e] = vv[e] + base;
+          float v = run;
+          int f = seen;
+          warp_pair_scan(v, f, lane);
+          float ve = __shfl_up_sync(kFull, v, 1);
+          int fe = __shfl_up_sync(kFull, f, 1);
+          if (lane == 0) {
+            ve = 0.f;
+            fe = 0;
           }
+          if (lane == 31) {
+            misc->pv[par][qd] = v;
+            misc->pf[par][qd] = f;
+          }
+          ptx::named_bar_sync(kEpiBar, kEpiThreads);
+          float wv = 0.f, tv = 0.f;
+          int wf = 0, tf = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float yv = misc->pv[par][k];
+            const int yf = misc->pf[par][k];
+            if (k < qd) compose(wv, wf, yv, yf);
+            compose(tv, tf, yv, yf);
+          }
+          compose(wv, wf, ve, fe);
+          double tprefix;
+          if constexpr (MODE == MODE_GENERAL) {
+            tprefix = carry;
+            carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
+            qmod += p.step_mod;
+            qdiv += p.step_div;
+            if (qmod >= p.m) {
+              qmod -= p.m;
+              ++qdiv;
+            }
+          } else {
+            // decoupled look-back across tiles (huge segments)
+            const long long tq0 = t * static_cast<long long>(kTileRows) * GR;
+            const bool first_start = (tq0 % p.m == 0) && !(t == 0 && has_carry);
+            if (warp == 2) {
+              if (lane == 0) {
+                if (tf)
+                  publish(p, t, ep, 2, static_cast<double>(tv));
+                else if (!(t == 0 || first_start))
+                  publish(p, t, ep, 1, static_cast<double>(tv));
+              }
+              double pre;
+              if (t == 0)
+                pre = has_carry ? *p.carry_in : 0.0;
+              else if (first_start)
+                pre = 0.0;
+              else
+                pre = lookback(p, t, ep, lane);
+              if (lane == 0) {
+                const double incl = tf ? static_cast<double>(tv) : pre + static_cast<double>(tv);
+                if (!tf) publish(p, t, ep, 2, incl);
+                misc->lb_prefix[par] = pre;
+              }
+            }
+            ptx::named_bar_sync(kEpiBar, kEpiThreads);
+            tprefix = misc->lb_prefix[par];
+          }
+          const float cinf = wf ? wv : static_cast<float>(tprefix + static_cast<double>(wv));
+#pragma unroll
+          for (int j = 0; j < GR; ++j)
+            if (chain[j]) off[j] += cinf;
         }
-        uint8_t* stg = smem + C::OFF_OUT + par * C::OUT_BYTES;
+        // outputs: in-granule scan + granule offset (exclusive: shifted),
+        // produced chunk by chunk straight into the swizzled staging tile.
+        constexpr bool ONE_OFF = (MODE == MODE_ROWS || MODE == MODE_TILES);
+        const bool excl = p.exclusive != 0;
+        auto outv = [&](int e) -> float {
+          const float base = off[ONE_OFF ? 0 : e / G];
+          if (excl) return (e % G == 0) ? (base + 0.f) : (vv[e - 1] + base);
+          return vv[e] + base;
+        };
+        if (p.total_out && row == (p.n - 1) / kRow) {
+          const int k = static_cast<int>((p.n - 1) % kRow);
+          float incl = 0.f;
+#pragma unroll
+          for (int e = 0; e < 64; ++e)
+            if (e == k) incl = vv[e] + off[ONE_OFF ? 0 : e / G];
+          *p.total_out = static_cast<double>(incl);
+        }
+        uint8_t* stg = smem + C::OFF_OUT + (C::OUT_BUFS == 2 ? par : 0) * C::OUT_BYTES;
         const uint32_t rb = static_cast<uint32_t>(rit) * 128u;
         const uint32_t sw = static_cast<uint32_t>(rit & 7);
         if constexpr (sizeof(OutT) == 2) {
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             uint4 w;
-            __half2 h0 = __floats2half2_rn(o[8 * c + 0], o[8 * c + 1]);
-            __half2 h1 = __floats2half2_rn(o[8 * c + 2], o[8 * c + 3]);
-            __half2 h2 = __floats2half2_rn(o[8 * c + 4], o[8 * c + 5]);
-            __half2 h3 = __floats2half2_rn(o[8 * c + 6], o[8 * c + 7]);
+            __half2 h0 = __floats2half2_rn(outv(8 * c + 0), outv(8 * c + 1));
+            __half2 h1 = __floats2half2_rn(outv(8 * c + 2), outv(8 * c + 3));
+            __half2 h2 = __floats2half2_rn(outv(8 * c + 4), outv(8 * c + 5));
+            __half2 h3 = __floats2half2_rn(outv(8 * c + 6), outv(8 * c + 7));
             w.x = *reinterpret_cast<uint32_t*>(&h0);
             w.y = *reinterpret_cast<uint32_t*>(&h1);
             w.z = *reinterpret_cast<uint32_t*>(&h2);
@@ -631,17 +856,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int h = 0; h < 2; ++h) {
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-              float4 w = make_float4(o[32 * h + 4 * c + 0], o[32 * h + 4 * c + 1],
-                                     o[32 * h + 4 * c + 2], o[32 * h + 4 * c + 3]);
+              float4 w = make_float4(outv(32 * h + 4 * c + 0), outv(32 * h + 4 * c + 1),
+                                     outv(32 * h + 4 * c + 2), outv(32 * h + 4 * c + 3));
               *reinterpret_cast<float4*>(stg + h * 16384 + rb + ((c ^ sw) << 4)) = w;
             }
           }
         }
         if (row == p.rows_full) {  // ragged last row is outside the TMA view: direct stores
           OutT* out = reinterpret_cast<OutT*>(p.out);
+#pragma unroll
           for (int k = 0; k < 64; ++k) {
             const long long e = row * kRow + k;
-            if (e < p.n) out[e] = cvt_out<OutT>(o[k]);
+            if (e < p.n) out[e] = cvt_out<OutT>(outv(k));
           }
         }
         ptx::fence_proxy_async_smem();
@@ -656,24 +882,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           ptx::bulk_commit();
         }
+        q0 += static_cast<long long>(kTileRows) * GR;
       }
     }  // tile loop
 
     if constexpr (OP == OP_SCAN) {
       if (leader) ptx::bulk_wait<0>();
     }
-    // ---- cross-CTA completion: reduce partial fixup / epoch bump
-    const bool need_ticket = (OP == OP_REDUCE) ? (p.need_fixup != 0) : (p.need_lookback != 0);
+    // ---- cross-CTA completion: reduce partial fixup / look-back epoch bump
+    const bool need_ticket = (OP == OP_REDUCE) ? (p.need_fixup != 0) : (MODE == MODE_LOOKBACK);
     if (need_ticket) {
       ptx::named_bar_sync(kEpiBar, kEpiThreads);
       if (leader) {
         if constexpr (OP == OP_REDUCE) {
           // open segment at the end of the range -> tail partial
-          const long long lg_end = t_end * (long long)kTileRows * GR;  // one past range's last granule
+          const long long lg_end = t_end * static_cast<long long>(kTileRows) * GR;
           const long long lg = (lg_end < p.qlast + 1 ? lg_end : p.qlast + 1) - 1;
           const bool closed = ((lg + 1) % p.m == 0) || (lg == p.qlast);
           Entry e0{misc->head_seg, misc->head_val};
-          Entry e1{closed ? -1LL : lg / p.m, tile_carry};
+          Entry e1{closed ? -1LL : lg / p.m, carry};
           p.entries[2 * cta] = e0;
           p.entries[2 * cta + 1] = e1;
         }
@@ -813,16 +1040,16 @@ static size_t ws_need(int op, long long n, long long seg) {
   return (b + 255) & ~size_t(255);
 }
 
-template <int OP, int GR, typename OutT>
+template <int OP, int GR, int MODE, typename OutT>
 static int launch(const Params& p0, int out_esize, cudaStream_t st) {
-  using C = Cfg<OP, GR, OutT>;
-  constexpr uint32_t smem = smem_bytes<OP, GR, OutT>();
-  auto kern = seg_kernel<OP, GR, OutT>;
+  constexpr uint32_t smem = smem_bytes<OP, GR, MODE, OutT>();
+  static_assert(smem <= 232448, "shared memory budget");
+  auto kern = seg_kernel<OP, GR, MODE, OutT>;
   static std::atomic<int> attr_done{0};
   if (!attr_done.load()) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
         cudaSuccess) {
-      set_err("cudaFuncSetAttribute failed: %s", cudaGetErrorString(cudaGetLastError()));
+      set_err("cudaFuncSetAttribute failed: %s%lld", cudaGetErrorString(cudaGetLastError()), 0);
       return TC_CUDA_ERROR;
     }
     attr_done.store(1);
@@ -838,16 +1065,16 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) !=
           cudaSuccess ||
       per_sm < 1) {
-    set_err("occupancy query failed: %s", cudaGetErrorString(cudaGetLastError()));
+    set_err("occupancy query failed: %s%lld", cudaGetErrorString(cudaGetLastError()), 0);
     return TC_CUDA_ERROR;
   }
+  if (per_sm > Cfg<OP, GR, MODE, OutT>::MINB) per_sm = Cfg<OP, GR, MODE, OutT>::MINB;
   long long grid = static_cast<long long>(di.sms) * per_sm;
   if (grid > p0.num_tiles) grid = p0.num_tiles;
   if (grid > kMaxCtas) grid = kMaxCtas;
   if (grid < 1) grid = 1;
 
-  Params p = p0;
-  // tensor maps
+  const Params& p = p0;
   CUtensorMap tin, tout;
   const char* wsb = reinterpret_cast<const char*>(p.hdr);
   const void* in_base = p.rows_full > 0 ? static_cast<const void*>(p.x)
@@ -878,7 +1105,7 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   int na = 0;
-  if (OP == OP_SCAN && p.need_lookback) {
+  if (MODE == MODE_LOOKBACK) {
     // decoupled look-back needs every CTA resident: cooperative launch
     // guarantees co-residency (or fails loudly instead of deadlocking).
     attr[0].id = cudaLaunchAttributeCooperative;
@@ -898,16 +1125,30 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
 
 using LaunchFn = int (*)(const Params&, int, cudaStream_t);
 
-template <int OP, typename OutT>
-static LaunchFn pick(int gr) {
+template <int OP, int MODE, typename OutT>
+static LaunchFn pick_gr(int gr) {
   switch (gr) {
-    case 1: return &launch<OP, 1, OutT>;
-    case 2: return &launch<OP, 2, OutT>;
-    case 4: return &launch<OP, 4, OutT>;
-    case 8: return &launch<OP, 8, OutT>;
-    case 16: return &launch<OP, 16, OutT>;
-    case 32: return &launch<OP, 32, OutT>;
-    case 64: return &launch<OP, 64, OutT>;
+    case 1: return &launch<OP, 1, MODE, OutT>;
+    case 2: return &launch<OP, 2, MODE, OutT>;
+    case 4: return &launch<OP, 4, MODE, OutT>;
+    case 8: return &launch<OP, 8, MODE, OutT>;
+    case 16: return &launch<OP, 16, MODE, OutT>;
+    case 32: return &launch<OP, 32, MODE, OutT>;
+    case 64: return &launch<OP, 64, MODE, OutT>;
+  }
+  return nullptr;
+}
+
+template <int OP, typename OutT>
+static LaunchFn pick(int gr, int mode) {
+  switch (mode) {
+    case MODE_LOCAL: return pick_gr<OP, MODE_LOCAL, OutT>(gr);
+    case MODE_ROWS: return gr == 1 ? &launch<OP, 1, MODE_ROWS, OutT> : nullptr;
+    case MODE_TILES: return gr == 1 ? &launch<OP, 1, MODE_TILES, OutT> : nullptr;
+    case MODE_GENERAL: return pick_gr<OP, MODE_GENERAL, OutT>(gr);
+    case MODE_LOOKBACK:
+      if constexpr (OP == OP_SCAN) return pick_gr<OP, MODE_LOOKBACK, OutT>(gr);
+      return nullptr;
   }
   return nullptr;
 }
@@ -942,13 +1183,13 @@ static int common_checks(const void* x, long long n, long long seg, const void* 
   return TC_OK;
 }
 
-static Params make_params(const void* x, long long n, long long seg, void* out, void* ws,
-                          int* gr_out) {
+// Segment geometry -> granules, carry mode and per-mode constants.
+static Params make_params(const void* x, long long n, long long seg, void* out, void* ws, int op,
+                          bool has_carry, int* gr_out, int* mode_out) {
   if (seg > n) seg = n;  // one segment spanning everything: same result, smaller m
   Params p{};
   const long long g = gcd_ll(seg, kRow);
   const int gr = static_cast<int>(kRow / g);
-  *gr_out = gr;
   p.x = reinterpret_cast<const __half*>(x);
   p.out = out;
   p.n = n;
@@ -957,6 +1198,31 @@ static Params make_params(const void* x, long long n, long long seg, void* out, 
   p.rows_full = n / kRow;
   p.num_tiles = (n + kTileElems - 1) / kTileElems;
   p.qlast = (n - 1) / g;
+  p.nseg = (n + seg - 1) / seg;
+  const long long step = static_cast<long long>(kTileRows) * gr;
+  p.step_div = step / p.m;
+  p.step_mod = step % p.m;
+  const bool scan_carry = (op == TC_OP_SCAN && has_carry);
+  int mode;
+  const bool pow2m = (p.m & (p.m - 1)) == 0;
+  if (p.m == 1 && !scan_carry) {
+    mode = MODE_LOCAL;
+  } else if (gr == 1 && pow2m && p.m <= kTileRows && !scan_carry) {
+    mode = MODE_ROWS;
+    int l = 0;
+    while ((1LL << l) < p.m) ++l;
+    p.log2m = l;
+  } else if (gr == 1 && p.m % kTileRows == 0 && !scan_carry) {
+    mode = MODE_TILES;
+    p.ktiles = p.m / kTileRows;
+  } else {
+    mode = MODE_GENERAL;
+  }
+  if (op == TC_OP_SCAN && (mode == MODE_TILES || mode == MODE_GENERAL) &&
+      (seg > kScanPrepassMax || scan_carry))
+    mode = MODE_LOOKBACK;
+  *gr_out = gr;
+  *mode_out = mode;
   char* w = reinterpret_cast<char*>(ws);
   p.hdr = reinterpret_cast<WsHeader*>(w);
   p.entries = reinterpret_cast<Entry*>(w + kWsEntries);
@@ -966,7 +1232,10 @@ static Params make_params(const void* x, long long n, long long seg, void* out, 
   p.lb_agg = reinterpret_cast<double*>(w + off);
   off += static_cast<size_t>(T) * 8;
   p.lb_inc = reinterpret_cast<double*>(w + off);
-  p.need_fixup = (kTileElems % seg != 0) ? 1 : 0;
+  p.need_fixup = (op == TC_OP_REDUCE && (mode == MODE_TILES || mode == MODE_GENERAL) &&
+                  (kTileElems % seg != 0))
+                     ? 1
+                     : 0;
   return p;
 }
 
@@ -989,18 +1258,18 @@ int tc_seg_reduce(const void* x, int64_t n, int64_t seg, void* out, int out_dtyp
   g_err[0] = 0;
   int rc = common_checks(x, n, seg, out, out_dtype, false, ws, ws_bytes, TC_OP_REDUCE);
   if (rc) return rc;
-  int gr = 0;
-  Params p = make_params(x, n, seg, out, ws, &gr);
+  int gr = 0, mode = 0;
+  Params p = make_params(x, n, seg, out, ws, TC_OP_REDUCE, false, &gr, &mode);
   LaunchFn fn = nullptr;
   int es = 2;
   if (out_dtype == TC_F16) {
-    fn = pick<OP_REDUCE, __half>(gr);
+    fn = pick<OP_REDUCE, __half>(gr, mode);
     es = 2;
   } else if (out_dtype == TC_F32) {
-    fn = pick<OP_REDUCE, float>(gr);
+    fn = pick<OP_REDUCE, float>(gr, mode);
     es = 4;
   } else {
-    fn = pick<OP_REDUCE, double>(gr);
+    fn = pick<OP_REDUCE, double>(gr, mode);
     es = 8;
   }
   if (!fn) {
@@ -1021,13 +1290,13 @@ int tc_seg_scan(const void* x, int64_t n, int64_t seg, void* out, int out_dtype,
   g_err[0] = 0;
   int rc = common_checks(x, n, seg, out, out_dtype, true, ws, ws_bytes, TC_OP_SCAN);
   if (rc) return rc;
-  int gr = 0;
-  Params p = make_params(x, n, seg, out, ws, &gr);
+  int gr = 0, mode = 0;
+  Params p = make_params(x, n, seg, out, ws, TC_OP_SCAN, carry_in != nullptr, &gr, &mode);
   p.exclusive = exclusive ? 1 : 0;
   p.carry_in = carry_in;
   p.total_out = total_out;
-  p.need_lookback = ((kTileElems % p.seg) != 0 || carry_in != nullptr) ? 1 : 0;
-  LaunchFn fn = (out_dtype == TC_F16) ? pick<OP_SCAN, __half>(gr) : pick<OP_SCAN, float>(gr);
+  LaunchFn fn =
+      (out_dtype == TC_F16) ? pick<OP_SCAN, __half>(gr, mode) : pick<OP_SCAN, float>(gr, mode);
   if (!fn) {
     set_err("no kernel for granules-per-row %s%lld", "", gr);
     return TC_BAD_CONFIG;

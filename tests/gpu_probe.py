@@ -63,8 +63,9 @@ def main():
     rng = np.random.default_rng(1)
     fails = 0
     total = 0
-    ns = [8192, 65536, 1 << 20, 1000, 100, 12345, 64, 8192 * 3 + 70]
-    segs = [16, 32, 64, 128, 256, 1024, 8192, 16384, 65536, 48, 300, 7, 1]
+    ns = [8192, 65536, 1 << 20, 1000, 100, 12345, 64, 8192 * 3 + 70, (1 << 22) + 1234]
+    segs = [16, 32, 64, 128, 256, 1024, 8192, 16384, 65536, 48, 300, 7, 1, 24576, 100000,
+            1 << 17, (1 << 18) + 8192, 1 << 20]
     only = sys.argv[1] if len(sys.argv) > 1 else "all"
     for n in ns:
         x = rng.integers(0, 8, n).astype(np.float16)
