@@ -224,7 +224,11 @@ def test_config3_scan_2p30_properties(s, cuda):
     red = D.seg_reduce(xd, s, torch.float32)
     tails = inc.view(-1, s)[:, -1]
     assert torch.allclose(tails.double(), red.double(), rtol=2e-6, atol=0)
-    assert torch.equal(exc.view(-1, s)[:, 1:], inc.view(-1, s)[:, :-1])
+    # exclusive == shifted inclusive: bit-exact on exact-integer data (matrix
+    # test above); on float data the two are rounded through different
+    # (equally accurate) associations at row boundaries
+    assert torch.allclose(exc.view(-1, s)[:, 1:].double(), inc.view(-1, s)[:, :-1].double(),
+                          rtol=2e-6, atol=0)
     assert torch.all(exc.view(-1, s)[:, 0] == 0)
     rs = np.random.default_rng(s)
     segs = rs.integers(0, n // s, 64)
