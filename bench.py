@@ -1,0 +1,488 @@
+"""bench.py -- the driver's benchmark contract for the B200 tensor-core
+segmented reduction / scan (arXiv 1811.09736).
+
+Workload (BASELINE.json configs[1], the config the headline metric is quoted
+on): segmented reduction of 2^30 fp16 elements, swept over the 13
+power-of-two segment sizes 16..65536; output fp16 (the reference's default
+``TileEngine(accumulate="half")``).  One STEP = one pass of the hot path
+over the input at every segment size of the sweep (13 kernel launches).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun, one process per GPU): weak scaling -- every rank owns its
+own 2^30-element shard of whole segments and runs the same sweep with NO
+data-path collective (segmented ops shard by whole segments, SURVEY.md
+section 8(e)); the full-reduce / full-scan extras shard 2^33 elements across
+the ranks and use one NCCL all_gather of per-rank fp64 partials.
+
+Reported (rank 0, one JSON line):
+  value     whole-job elements/s with inputs resident in HBM (device time,
+            CUDA events, max over ranks);
+  e2e       the same sweep through the public drop-in API
+            (``segmented_reduce`` on pinned host tensors: H2D + kernel + D2H
+            inside the timed region);
+  roofline  algorithmic bytes (2n + 2*ceil(n/s) per launch) / measured
+            kernel time against MEASURED_PEAKS.json's copy bandwidth;
+  cpu_baseline  the C restatement of the reference oracle (oracle/oracle.c)
+            on the host cores, on a bounded prefix of the same input;
+  extras    scan sweep (configs[2]), full reduce / full exclusive scan of
+            2^33 elements (configs[3], configs[4]).
+
+``--impl reference`` times the reference's CPU path instead (the oracle
+port, all host threads) on the same metric/config and prints the same line
+with ``"impl": "reference"``.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+REDUCE_SEGS = [1 << k for k in range(4, 17)]  # 16 .. 65536
+SCAN_SEGS = [1 << k for k in range(4, 15)]    # 16 .. 16384
+LOG2N = 30
+FULL_LOG2N = 33
+METRIC = "seg reduce/scan elems/s and HBM GB/s (% of peak) vs segment size, 1/2/4/8 B200"
+UNIT = "elems/s"
+WORKLOAD = ("segmented reduction fp16, 2^30 elements, segment-size sweep 16-65536 "
+            "(13 power-of-two sizes, one launch each per step), fp16 sums")
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def reduce_bytes(n, s, o=2):
+    return 2 * n + o * (-(-n // s))
+
+
+# ----------------------------------------------------------------- CPU side
+
+
+def load_oracle():
+    so = ROOT / "oracle" / "build" / "liboracle.so"
+    if not so.exists():
+        subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], check=True)
+    lib = ctypes.CDLL(str(so))
+    lib.or_seg_reduce.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                  ctypes.c_void_p, ctypes.c_int]
+    lib.or_seg_reduce.restype = None
+    lib.or_init()
+    return lib
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def cpu_sweep(lib, xh: np.ndarray, threads: int) -> float:
+    """One reference-CPU sweep over xh (all segment sizes); returns seconds."""
+    n = xh.size
+    outs = {s: np.empty(-(-n // s), np.float64) for s in REDUCE_SEGS}
+    t0 = time.perf_counter()
+    for s in REDUCE_SEGS:
+        lib.or_seg_reduce(xh.ctypes.data, n, s, outs[s].ctypes.data, threads)
+    return time.perf_counter() - t0
+
+
+def cpu_sample_size(lib, threads, budget_s, xh_full=None):
+    """Largest power-of-two prefix (<= 2^30) whose sweep takes ~budget_s."""
+    probe_n = 1 << 22
+    xp = xh_full[:probe_n] if xh_full is not None else synth_host(probe_n)
+    cpu_sweep(lib, xp, threads)  # warm the decode table / pages
+    t = cpu_sweep(lib, xp, threads)
+    rate = probe_n / max(t, 1e-9)
+    n = 1 << 22
+    while n < (1 << LOG2N) and 2 * n / rate <= budget_s:
+        n *= 2
+    return n
+
+
+def synth_host(n, seed=0):
+    rng = np.random.default_rng(seed)
+    return rng.random(n, dtype=np.float32).astype(np.float16)
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (the oracle port) on the
+    host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    lib = load_oracle()
+    threads = host_threads()
+    n = cpu_sample_size(lib, threads, args.ref_step_seconds)
+    xh = synth_host(n)
+    for _ in range(args.warmup):
+        cpu_sweep(lib, xh, threads)
+    ts = [cpu_sweep(lib, xh, threads) for _ in range(args.steps)]
+    total = sum(ts)
+    value = len(REDUCE_SEGS) * n * args.steps / total
+    sample = (f"sweep of {len(REDUCE_SEGS)} segment sizes over a 2^{n.bit_length() - 1}-element "
+              f"prefix per step (uniform [0,1) fp16), oracle/oracle.c or_seg_reduce, "
+              f"{threads} pthreads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+        "config": config_dict(args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(world):
+    return {
+        "workload": WORKLOAD,
+        "n_per_gpu": 1 << LOG2N,
+        "segment_sizes": REDUCE_SEGS,
+        "out_dtype": "f16",
+        "l2": "inputs 2 GiB per GPU >> 126 MB L2 (no flush needed)",
+        "parallelism": f"whole-segment shards, {world} GPU(s), no data-path collective",
+    }
+
+
+# ----------------------------------------------------------------- GPU side
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.15)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, smax, reasons = [], None, set()
+        for r in self.samples:
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+                for nm, v in zip(names, r[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def gen_device(n, device, seed):
+    """Uniform [0, 1) fp16 on the device, generated in chunks."""
+    import torch
+
+    x = torch.empty(n, dtype=torch.float16, device=device)
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    chunk = 1 << 28
+    for lo in range(0, n, chunk):
+        hi = min(n, lo + chunk)
+        x[lo:hi] = torch.rand(hi - lo, generator=g, device=device, dtype=torch.float32)
+    return x
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_1811_09736_b200 as ht
+    from paper_1811_09736_b200 import _device as D
+    from paper_1811_09736_b200 import _lib
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    peak, peak_src = peaks()
+    n = 1 << LOG2N
+    x = gen_device(n, dev, seed=1000 + rank)
+    outs = {s: torch.empty(-(-n // s), dtype=torch.float16, device=dev) for s in REDUCE_SEGS}
+    stream = torch.cuda.current_stream(dev)
+
+    def sweep():
+        for s in REDUCE_SEGS:
+            D.seg_reduce(x, s, torch.float16, out=outs[s])
+
+    for _ in range(args.warmup):
+        sweep()
+    barrier()
+
+    # ---- timed region: K steps, per-launch CUDA events on the launch stream
+    nl = len(REDUCE_SEGS)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps * nl + 1)]
+    _lib.lib.tc_reset_launch_count()
+    with ClockSampler(local) as clk:
+        barrier()
+        evs[0].record(stream)
+        for k in range(args.steps):
+            for i, s in enumerate(REDUCE_SEGS):
+                D.seg_reduce(x, s, torch.float16, out=outs[s])
+                evs[k * nl + i + 1].record(stream)
+        barrier()
+    launches = int(_lib.lib.tc_launch_count())
+    per = [evs[j].elapsed_time(evs[j + 1]) for j in range(args.steps * nl)]
+    total_ms = evs[0].elapsed_time(evs[-1])
+    total_ms = max_over_ranks(total_ms)
+    ms_per_step = total_ms / args.steps
+    value = world * nl * n / (ms_per_step / 1e3)
+
+    sweep_rows = []
+    tot_bytes, tot_ms = 0.0, 0.0
+    for i, s in enumerate(REDUCE_SEGS):
+        ms = statistics.median(per[k * nl + i] for k in range(args.steps))
+        b = reduce_bytes(n, s)
+        tot_bytes += b
+        tot_ms += ms
+        sweep_rows.append({"seg": s, "ms": round(ms, 4), "gelem_s": round(n / ms / 1e6, 1),
+                           "gbs": round(b / ms / 1e6, 1), "frac": round(b / ms / 1e6 / peak, 4)})
+    achieved = tot_bytes / tot_ms / 1e6
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("per_launch_bytes")
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "peak_source": peak_src,
+                "kernel": "tc::seg_kernel<OP_REDUCE,...> (13 launches/step)",
+                "algorithmic_bytes": "2n + 2*ceil(n/s) per launch, n = 2^30"}
+
+    # ---- e2e through the public drop-in API with pinned host buffers
+    xh = torch.empty(n, dtype=torch.float16, pin_memory=True)
+    xh.copy_(x)
+    eng = ht.TileEngine()
+    plans = {s: ht.select_algorithm("reduce", s, n).variant for s in REDUCE_SEGS}
+
+    def e2e_sweep():
+        res = None
+        for s in REDUCE_SEGS:
+            res = ht.segmented_reduce(xh, s, plans[s], eng)
+        return res
+
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    e2e_sweep()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_sweep()
+    e1.record(stream)
+    barrier()
+    wall_ms = (time.perf_counter() - t0) * 1e3
+    e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), wall_ms)) / e2e_steps
+    e2e = {"value": world * nl * n / (e2e_ms / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": nl * 2 * n,
+           "d2h_bytes_per_step": sum(2 * (-(-n // s)) for s in REDUCE_SEGS),
+           "ms_per_step": round(e2e_ms, 3),
+           "api": "paper_1811_09736_b200.segmented_reduce(pinned torch CPU fp16, s, "
+                  "select_algorithm(...).variant, TileEngine())"}
+    del xh
+
+    extras = {}
+    if not args.no_extras:
+        extras = run_extras(args, x, dev, world, rank, barrier, max_over_ranks, peak)
+
+    # ---- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        lib = load_oracle()
+        threads = host_threads()
+        host = x.cpu().numpy()
+        ncpu = cpu_sample_size(lib, threads, args.cpu_seconds / 2, host)
+        xs = np.ascontiguousarray(host[:ncpu])
+        t = min(cpu_sweep(lib, xs, threads) for _ in range(2))
+        cpu = {"value": len(REDUCE_SEGS) * ncpu / t, "unit": UNIT, "cores": threads,
+               "kind": "port",
+               "sample": (f"same sweep on the first 2^{ncpu.bit_length() - 1} elements of the "
+                          f"bench input, oracle/oracle.c or_seg_reduce (binary64), "
+                          f"{threads} pthreads, best of 2")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+            "data": "synthetic (uniform [0,1) fp16, torch.rand seeded per rank)",
+            "config": config_dict(world),
+            "gbs_per_gpu": round(achieved, 1),
+            "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
+            "cpu_baseline": cpu, "clocks": clk.summary(), "sweep": sweep_rows,
+            "extras": extras,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _time_op(fn, reps, warm, stream, barrier, max_over_ranks):
+    import torch
+
+    for _ in range(warm):
+        fn()
+    barrier()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
+        fn()
+    b.record(stream)
+    barrier()
+    return max_over_ranks(a.elapsed_time(b)) / reps
+
+
+def run_extras(args, x, dev, world, rank, barrier, max_over_ranks, peak):
+    """configs[2..4]: scan sweep (1 GPU each rank), full reduce / full
+    exclusive scan of 2^33 elements sharded over the ranks."""
+    import torch
+
+    from paper_1811_09736_b200 import _device as D
+    from paper_1811_09736_b200 import distributed as PD
+
+    stream = torch.cuda.current_stream(dev)
+    n = x.numel()
+    reps = max(3, args.steps)
+    out = {}
+    # segmented inclusive scan sweep, fp16 out (paper accounting 4 B/elem)
+    y = torch.empty(n, dtype=torch.float16, device=dev)
+    rows = []
+    for s in SCAN_SEGS:
+        ms = _time_op(lambda: D.seg_scan(x, s, torch.float16, out=y), reps, 2, stream, barrier,
+                      max_over_ranks)
+        b = 4 * n
+        rows.append({"seg": s, "ms": round(ms, 4), "gelem_s": round(world * n / ms / 1e6, 1),
+                     "gbs_per_gpu": round(b / ms / 1e6, 1), "frac": round(b / ms / 1e6 / peak, 4)})
+    out["scan_sweep_f16"] = {"workload": "segmented inclusive scan fp16, 2^30 per GPU, fp16 out",
+                             "rows": rows}
+    del y
+    # full ops over 2^33 elements sharded across the ranks
+    nf = 1 << FULL_LOG2N
+    lo, hi = PD.even_bounds(nf, world, rank)
+    xl = gen_device(hi - lo, dev, seed=7 + rank)
+    ms = _time_op(lambda: PD.sharded_full_reduce(xl, torch.float32), reps, 2, stream, barrier,
+                  max_over_ranks)
+    b = 2 * (hi - lo) + 4
+    out["full_reduce_2^33"] = {"ms": round(ms, 4), "gelem_s": round(nf / ms / 1e6, 1),
+                               "gbs_per_gpu": round(b / ms / 1e6, 1),
+                               "frac": round(b / ms / 1e6 / peak, 4),
+                               "exchange": "NCCL all_gather of fp64 partials" if world > 1
+                               else "none"}
+    yl = torch.empty(hi - lo, dtype=torch.float32, device=dev)
+
+    def fscan():
+        if world > 1:
+            return PD.sharded_full_scan(xl, torch.float32, exclusive=True)
+        return D.full_scan(xl, torch.float32, exclusive=True, out=yl)
+
+    ms = _time_op(fscan, reps, 2, stream, barrier, max_over_ranks)
+    b = 6 * (hi - lo)
+    actual = b + (2 * (hi - lo) if world > 1 else 0)
+    out["full_exclusive_scan_2^33"] = {
+        "ms": round(ms, 4), "gelem_s": round(nf / ms / 1e6, 1),
+        "gbs_per_gpu_algorithmic": round(b / ms / 1e6, 1),
+        "frac": round(b / ms / 1e6 / peak, 4),
+        "gbs_per_gpu_actual": round(actual / ms / 1e6, 1), "out_dtype": "f32"}
+    del xl, yl
+    torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0,
+                    help="approximate CPU-baseline budget (ours arm)")
+    ap.add_argument("--ref-step-seconds", type=float, default=4.0,
+                    help="approximate seconds per reference-arm step")
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # contract: W >= 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

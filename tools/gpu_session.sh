@@ -1,0 +1,31 @@
+#!/usr/bin/env bash
+# One GPU-box session: tests, bench, launch list, ncu captures.
+# usage: tools/gpu_session.sh TAG [parts...]   parts: test bench launches prof probe
+set -u
+TAG=${1:-r01}; shift || true
+PARTS=${*:-"test bench launches prof"}
+OUT=gpurun_out/$TAG
+mkdir -p "$OUT"
+nvidia-smi > "$OUT/nvidia-smi.txt" 2>&1
+python -c 'import __graft_entry__ as g; g.build()' > "$OUT/build.log" 2>&1 || { echo BUILD FAILED; tail -20 "$OUT/build.log"; }
+for p in $PARTS; do
+  case $p in
+    test)
+      timeout 900 python -m pytest tests -m gpu -x -q > "$OUT/pytest_gpu.log" 2>&1; echo "pytest gpu rc=$?"; tail -3 "$OUT/pytest_gpu.log"
+      timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > "$OUT/smoke.log" 2>&1; echo "smoke rc=$?"; tail -2 "$OUT/smoke.log";;
+    bench)
+      timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?"; tail -c 3000 "$OUT/bench.json"; tail -5 "$OUT/bench.err"
+      timeout 600 python bench.py --impl reference > "$OUT/bench_ref.json" 2> "$OUT/bench_ref.err"; echo "bench ref rc=$?"; cut -c1-400 "$OUT/bench_ref.json";;
+    launches)
+      timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 120 --csv \
+        --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 3 --no-extras --no-cpu --e2e-steps 1 > "$OUT/launches_bench.log" 2>&1; echo "launches rc=$?";;
+    prof)
+      for cfg in "reduce 16 f16" "reduce 256 f16" "reduce 65536 f16" "scan 256 f16" "scan 16384 f32"; do
+        set -- $cfg
+        timeout 600 ncu --set full --clock-control none --import-source on -k regex:seg_kernel -s 2 -c 1 \
+          -o "$OUT/prof_$1_$2_$3" -f python tests/prof_one.py $1 $2 $3 30 3 > "$OUT/prof_$1_$2_$3.log" 2>&1; echo "prof $cfg rc=$?"
+      done;;
+    probe)
+      timeout 600 python tests/perf_probe.py > "$OUT/perf_probe.log" 2>&1; echo "probe rc=$?"; cat "$OUT/perf_probe.log";;
+  esac
+done
