@@ -434,8 +434,12 @@ def run_extras(args, x, dev, world, rank, barrier, max_over_ranks, peak):
     nf = 1 << FULL_LOG2N
     lo, hi = PD.even_bounds(nf, world, rank)
     xl = gen_device(hi - lo, dev, seed=7 + rank)
-    ms = _time_op(lambda: PD.sharded_full_reduce(xl, torch.float32), reps, 2, stream, barrier,
-                  max_over_ranks)
+    def freduce():
+        if world > 1:
+            return PD.sharded_full_reduce(xl, torch.float32)
+        return D.full_reduce(xl, torch.float32)
+
+    ms = _time_op(freduce, reps, 2, stream, barrier, max_over_ranks)
     b = 2 * (hi - lo) + 4
     out["full_reduce_2^33"] = {"ms": round(ms, 4), "gelem_s": round(nf / ms / 1e6, 1),
                                "gbs_per_gpu": round(b / ms / 1e6, 1),
