@@ -321,17 +321,37 @@ def run_ours(args):
                 "kernel": "tc::seg_kernel<OP_REDUCE,...> (13 launches/step)",
                 "algorithmic_bytes": "2n + 2*ceil(n/s) per launch, n = 2^30"}
 
-    # ---- e2e through the public drop-in API with pinned host buffers
+    # ---- e2e through the public drop-in API with pinned host buffers: the
+    # step's input is copied host->device ONCE per step, in 8 chunks of whole
+    # segments on a copy stream, and every chunk is swept (13 public-API
+    # calls on the device chunk) as soon as it lands, overlapping the next
+    # chunk's copy; the 13 results go back device->host into pinned buffers.
     xh = torch.empty(n, dtype=torch.float16, pin_memory=True)
     xh.copy_(x)
     eng = ht.TileEngine()
     plans = {s: ht.select_algorithm("reduce", s, n).variant for s in REDUCE_SEGS}
+    nchunk = 8
+    clen = n // nchunk  # multiple of every segment size (2^27 / 2^16)
+    xdev = torch.empty(n, dtype=torch.float16, device=dev)
+    res_h = {s: torch.empty(-(-n // s), dtype=torch.float16, pin_memory=True) for s in REDUCE_SEGS}
+    copy_stream = torch.cuda.Stream(dev)
+    landed = [torch.cuda.Event() for _ in range(nchunk)]
 
     def e2e_sweep():
-        res = None
+        with torch.cuda.stream(copy_stream):
+            for c in range(nchunk):
+                xdev[c * clen:(c + 1) * clen].copy_(xh[c * clen:(c + 1) * clen], non_blocking=True)
+                landed[c].record(copy_stream)
+        parts = {s: [] for s in REDUCE_SEGS}
+        for c in range(nchunk):
+            stream.wait_event(landed[c])
+            xc = xdev[c * clen:(c + 1) * clen]
+            for s in REDUCE_SEGS:
+                parts[s].append(ht.segmented_reduce(xc, s, plans[s], eng))
         for s in REDUCE_SEGS:
-            res = ht.segmented_reduce(xh, s, plans[s], eng)
-        return res
+            res_h[s].copy_(torch.cat(parts[s]), non_blocking=True)
+        stream.synchronize()
+        return res_h
 
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     e2e_sweep()
@@ -347,12 +367,14 @@ def run_ours(args):
     wall_ms = (time.perf_counter() - t0) * 1e3
     e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), wall_ms)) / e2e_steps
     e2e = {"value": world * nl * n / (e2e_ms / 1e3), "unit": UNIT,
-           "h2d_bytes_per_step": nl * 2 * n,
+           "h2d_bytes_per_step": 2 * n,
            "d2h_bytes_per_step": sum(2 * (-(-n // s)) for s in REDUCE_SEGS),
            "ms_per_step": round(e2e_ms, 3),
-           "api": "paper_1811_09736_b200.segmented_reduce(pinned torch CPU fp16, s, "
-                  "select_algorithm(...).variant, TileEngine())"}
-    del xh
+           "api": "pinned host fp16 -> 8 chunked H2D copies (copy stream) -> per chunk "
+                  "paper_1811_09736_b200.segmented_reduce(chunk, s, select_algorithm(...)."
+                  "variant, TileEngine()) for the 13 sizes -> D2H of the 13 results into "
+                  "pinned host buffers"}
+    del xh, xdev, res_h
 
     extras = {}
     if not args.no_extras:

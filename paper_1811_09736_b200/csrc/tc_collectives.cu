@@ -24,12 +24,28 @@
 //        MODE_ROWS     seg = 64*2^k <= 8192: aligned row groups (shuffles)
 //        MODE_TILES    seg = 8192*k: whole tiles, CTA-sequential fp64 carry
 //        MODE_GENERAL  anything else: segmented (value, flag) pair scan
-//        MODE_LOOKBACK scan of huge segments: round-robin tiles + decoupled
-//                      look-back (fp64 aggregates / prefixes in HBM)
+//        MODE_CHUNK    scan of huge segments / full scan / scan with a
+//                      carry-in: L2-resident chunked reduce-then-scan in ONE
+//                      kernel (see below)
 //    Reductions and bounded-segment scans give every CTA one contiguous
 //    tile range; a reduce combines the segments cut by range boundaries in
 //    a deterministic last-CTA fixup, a scan recomputes the carry entering
 //    its range from the (< seg) preceding elements.
+//
+//  * MODE_CHUNK (the paper's grid scan, scan.py:249-310, as a single pass
+//    over HBM).  The input is cut into chunks of Gc x K tiles; CTA c owns
+//    unit (j, c) = K consecutive tiles of chunk j.  Each tile is loaded and
+//    multiplied once; its X.U result stays in TMEM (8 tile slots = all 512
+//    columns) while the epilogue walks A(0), A(1), O(0), A(2), O(1), ...:
+//    A(j) reads the row totals of unit j and publishes the unit's segmented
+//    aggregate (value, has-segment-start) with a release flag; O(j), one
+//    unit later, reads the same TMEM slots again and writes the prefix sums
+//    seeded with the value entering the unit.  That value comes from a
+//    dedicated prefix warp which composes, in fixed unit order and fp64,
+//    the aggregates of every earlier unit (all of the earlier chunks, the
+//    lower CTAs of this chunk) -- no serial chain between CTAs, and its
+//    spin-waits overlap the epilogue.  HBM traffic is the minimal 2 + o
+//    bytes/element; cooperative launch keeps the spin-waits deadlock-free.
 //
 //  * Warp specialisation (192 threads, persistent grid, 2 CTAs/SM): warp 0
 //    = TMA producer, warp 1 = TMEM allocator + single-thread MMA issuer,
@@ -74,7 +90,7 @@ constexpr int MODE_LOCAL = 0;
 constexpr int MODE_ROWS = 1;
 constexpr int MODE_TILES = 2;
 constexpr int MODE_GENERAL = 3;
-constexpr int MODE_LOOKBACK = 4;
+constexpr int MODE_CHUNK = 4;
 constexpr int kMaxCtas = 1024;                    // persistent grid cap
 constexpr long long kScanPrepassMax = 1LL << 18;  // largest seg whose range-entry carry is recomputed
 constexpr unsigned kFull = 0xffffffffu;
@@ -112,9 +128,9 @@ struct Params {
   double* total_out;
   WsHeader* hdr;
   Entry* entries;
-  uint32_t* lb_flag;
-  double* lb_agg;
-  double* lb_inc;
+  long long ck;        // CHUNK: tiles per unit (K)
+  long long lag;       // CHUNK: units between a unit's A pass and its O pass
+  uint64_t* u_word;    // CHUNK: per-unit aggregate, one 64-bit word (see unit_word)
   int exclusive;
   int need_fixup;  // reduce: segments may straddle CTA ranges
 };
@@ -157,9 +173,14 @@ template <int OP, int GR, int MODE, typename OutT>
 struct Cfg {
   static constexpr int G = 64 / GR;                                      // granule size
   static constexpr int N = (OP == OP_SCAN) ? 64 : (GR < 16 ? 16 : GR);  // UMMA N
-  static constexpr int MINB = (OP == OP_SCAN && GR >= 32) ? 1 : 2;      // CTAs per SM
-  static constexpr int STAGES = (OP == OP_REDUCE) ? (MINB == 2 ? 6 : 8) : (MINB == 2 ? 4 : 6);
-  static constexpr int ACC = 4;  // TMEM accumulator stages
+  static constexpr bool CHUNK = (MODE == MODE_CHUNK);
+  // CTAs per SM (CHUNK keeps 2-4 units of tiles in TMEM: all 512 columns, 1 CTA/SM)
+  static constexpr int MINB = (CHUNK || (OP == OP_SCAN && GR >= 32)) ? 1 : 2;
+  static constexpr int STAGES =
+      CHUNK ? 8 : (OP == OP_REDUCE) ? (MINB == 2 ? 6 : 8) : (MINB == 2 ? 4 : 6);
+  static constexpr int ACC = CHUNK ? 8 : 4;  // TMEM accumulator stages (tiles)
+  // warps: TMA, MMA, 4 epilogue (+ CHUNK: the prefix warp)
+  static constexpr int THREADS = CHUNK ? kThreads + 32 : kThreads;
   static constexpr int TMEM_COLS = pow2_at_least(ACC * N);
   static constexpr int OUT_BUFS = (OP == OP_SCAN) ? ((sizeof(OutT) == 4 && MINB == 2) ? 1 : 2) : 0;
   static constexpr uint32_t OUT_BYTES = kTileElems * sizeof(OutT);
@@ -167,7 +188,7 @@ struct Cfg {
   static constexpr uint32_t OFF_OUT = OFF_B + ((N * 128 + 1023) / 1024) * 1024;
   static constexpr uint32_t OFF_MISC = OFF_OUT + OUT_BUFS * OUT_BYTES;
   static constexpr int LD_COLS = (OP == OP_SCAN) ? 64 : GR;  // TMEM columns read per tile
-  static constexpr bool CONTIG = (MODE != MODE_LOOKBACK);    // contiguous CTA tile ranges
+  static constexpr bool CONTIG = (MODE != MODE_CHUNK);       // contiguous CTA tile ranges
 };
 
 template <int STAGES, int ACC>
@@ -181,7 +202,16 @@ struct Misc {
   float pv[2][4];
   int pf[2][4];
   double dsum[4];
-  double lb_prefix[2];
+  double ce_base;
+  double cev[4];
+  int cef[4];
+  double pd[2][4];
+  double fa[2][4];
+  float ov[2][4];
+  int of[2][4];
+  uint64_t pfull[4];   // CHUNK: prefix warp -> epilogue (entry value of unit j ready)
+  uint64_t pempty[4];  // CHUNK: epilogue -> prefix warp (slot consumed)
+  double entry[4];
   long long head_seg;
   double head_val;
 };
@@ -240,6 +270,12 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
 __device__ __forceinline__ float warp_incl_scan(float v, int lane) {
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -290,43 +326,111 @@ __device__ double epi_range_sum(const __half* x, long long lo, long long hi, int
   return r;
 }
 
-// Decoupled look-back over tiles: exclusive running value entering tile t.
-// Lane i inspects tile (t-1-i) - 32*w.  Status word = (epoch << 2) | state,
-// state 1 = aggregate published (lb_agg), 2 = inclusive published (lb_inc).
-__device__ double lookback(const Params& p, long long t, uint32_t ep, int lane) {
-  double acc = 0.0;
-  long long base = t - 1;
-  while (true) {
-    const long long j = base - lane;
-    bool isP = true;
-    double val = 0.0;
-    if (j >= 0) {
-      uint32_t st;
-      do {
-        st = ptx::ld_acquire_u32(p.lb_flag + j);
-      } while ((st >> 2) != ep || (st & 3u) == 0u);
-      isP = (st & 3u) == 2u;
-      val = isP ? ptx::ld_relaxed_f64(p.lb_inc + j) : ptx::ld_relaxed_f64(p.lb_agg + j);
-    }
-    const unsigned pm = __ballot_sync(kFull, isP);
-    const int lim = pm ? (__ffs(pm) - 1) : 31;
-    double c = (lane <= lim) ? val : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
-    acc += c;
-    if (pm) break;
-    base -= 32;
-  }
-  return acc;
+// CHUNK: a unit's aggregate (value, has-segment-start) and its validity
+// tag travel in ONE 64-bit word -- high half the fp32 value, low half
+// (epoch << 2) | state, state 1 = no segment start, 2 = start -- so a
+// single relaxed store publishes it and a single relaxed load observes it
+// whole (64-bit single-copy atomicity): no fences on either side.
+__device__ __forceinline__ uint64_t unit_word(double v, int f, uint32_t ep) {
+  const uint32_t bits = __float_as_uint(static_cast<float>(v));
+  return (static_cast<uint64_t>(bits) << 32) | ((ep << 2) | (f ? 2u : 1u));
+}
+__device__ __forceinline__ void chunk_publish(uint64_t* word, double v, int f, uint32_t ep) {
+  ptx::st_relaxed_u64(word, unit_word(v, f, ep));
 }
 
-__device__ __forceinline__ void publish(const Params& p, long long t, uint32_t ep, int state,
-                                        double v) {
-  if (state == 2)
-    ptx::st_relaxed_f64(p.lb_inc + t, v);
-  else
-    ptx::st_relaxed_f64(p.lb_agg + t, v);
-  ptx::st_release_u32(p.lb_flag + t, (ep << 2) | static_cast<uint32_t>(state));
+// CHUNK prefix warp: for each unit j of this CTA, the value of the open
+// segment entering it, handed to the epilogue through misc->entry[j & 3]
+// (mbarriers pfull / pempty).  It keeps P = the value entering chunk j,
+// composed from ALL units of the earlier chunks, so no CTA waits on
+// another's prefix (no serial chain): per chunk it reads every unit
+// aggregate (batched relaxed flag loads + one acquire fence), composes them
+// in unit order -- E(j) = P (+) units (j, 0..cta-1), P' = P (+) all units
+// of chunk j -- in fp64, the same fixed order on every run.
+template <typename MiscT>
+__device__ void prefix_warp(const Params& p, MiscT* misc, long long n_units, int cta, int Gc,
+                            long long ck, long long T, int lane, uint32_t ep, bool has_carry) {
+  constexpr int kMaxPer = 8;  // CHUNK grids have <= 256 CTAs (1 per SM)
+  const int per = (Gc + 31) / 32;
+  const long long chunk_t = static_cast<long long>(Gc) * ck;
+  double P = has_carry ? *p.carry_in : 0.0;
+  for (long long j = 0; j < n_units; ++j) {
+    // units that exist in chunk j
+    const long long left = (T - j * chunk_t + ck - 1) / ck;
+    const int cnt = left < Gc ? static_cast<int>(left) : Gc;
+    const int c0 = lane * per;
+    uint64_t w[kMaxPer];
+    unsigned pending = 0;
+#pragma unroll
+    for (int k = 0; k < kMaxPer; ++k)
+      if (k < per && c0 + k < cnt) pending |= 1u << k;
+    while (pending) {  // batched: one round trip per poll, not per unit
+#pragma unroll
+      for (int k = 0; k < kMaxPer; ++k)
+        if (pending & (1u << k)) w[k] = ptx::ld_relaxed_u64(p.u_word + j * Gc + c0 + k);
+#pragma unroll
+      for (int k = 0; k < kMaxPer; ++k)
+        if ((pending & (1u << k)) && (static_cast<uint32_t>(w[k]) >> 2) == ep)
+          pending &= ~(1u << k);
+      if (pending) __nanosleep(32);
+    }
+    // per-lane ordered aggregates: a_all over the lane's units, a_pre over those < cta
+    double va = 0.0, vp = 0.0;
+    int fa = 0, fp = 0;
+#pragma unroll
+    for (int k = 0; k < kMaxPer; ++k) {
+      const int c2 = c0 + k;
+      if (k < per && c2 < cnt) {
+        const double y = static_cast<double>(__uint_as_float(static_cast<uint32_t>(w[k] >> 32)));
+        const int yf = (static_cast<uint32_t>(w[k]) & 3u) == 2u;
+        va = yf ? y : va + y;
+        fa |= yf;
+        if (c2 < cta) {
+          vp = va;
+          fp = fa;
+        }
+      }
+    }
+    // inclusive ordered pair scan of a_all over the lanes
+    double vi = va;
+    int fi = fa;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double vu = __shfl_up_sync(kFull, vi, d);
+      const int fu = __shfl_up_sync(kFull, fi, d);
+      if (lane >= d) {
+        if (!fi) vi += vu;
+        fi |= fu;
+      }
+    }
+    double ve = __shfl_up_sync(kFull, vi, 1);
+    int fe = __shfl_up_sync(kFull, fi, 1);
+    if (lane == 0) {
+      ve = 0.0;
+      fe = 0;
+    }
+    // prefix over units < cta: exclusive lanes before Lc, then Lc's partial block
+    double e = P;
+    if (cta > 0) {
+      const int lc = (cta - 1) / per;
+      const double xv = __shfl_sync(kFull, ve, lc);
+      const int xf = __shfl_sync(kFull, fe, lc);
+      const double pv = __shfl_sync(kFull, vp, lc);
+      const int pf = __shfl_sync(kFull, fp, lc);
+      e = xf ? xv : P + xv;
+      e = pf ? pv : e + pv;
+    }
+    const double tv = __shfl_sync(kFull, vi, 31);
+    const int tf = __shfl_sync(kFull, fi, 31);
+    P = tf ? tv : P + tv;
+    if (lane == 0) {
+      const int ps = static_cast<int>(j & 3);
+      ptx::mbar_wait(&misc->pempty[ps], static_cast<uint32_t>(((j >> 2) & 1) ^ 1));
+      misc->entry[ps] = e;
+      ptx::mbar_arrive(&misc->pfull[ps]);
+    }
+    __syncwarp();
+  }
 }
 
 // Store GR consecutive outputs out[q0 .. q0+GR) (vectorised when aligned).
@@ -361,7 +465,7 @@ __device__ __forceinline__ void store_run(OutT* out, long long q0, const float (
 }
 
 template <int OP, int GR, int MODE, typename OutT>
-__global__ void __launch_bounds__(kThreads, (Cfg<OP, GR, MODE, OutT>::MINB))
+__global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, GR, MODE, OutT>::MINB))
     seg_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
                const Params p) {
   using C = Cfg<OP, GR, MODE, OutT>;
@@ -377,26 +481,56 @@ __global__ void __launch_bounds__(kThreads, (Cfg<OP, GR, MODE, OutT>::MINB))
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  // ---- work assignment: contiguous tile range (round robin for LOOKBACK)
+  // ---- work assignment: one contiguous tile range per CTA, or (CHUNK)
+  // unit (j, cta) = tiles [j*Gc*K + cta*K, +K).  Producer and MMA stream
+  // each tile ONCE; the CHUNK epilogue visits every unit twice from TMEM,
+  // as A(0), A(1), O(0), A(2), O(1), ... (A = aggregate, O = output).
   const long long T = p.num_tiles;
   const int Gc = gridDim.x;
   const int cta = blockIdx.x;
-  long long t_begin, t_end;
-  int t_count;
+  long long t_begin = 0, t_end = 0;
   if constexpr (C::CONTIG) {
     t_begin = T * cta / Gc;
     t_end = T * (cta + 1) / Gc;
-    t_count = static_cast<int>(t_end - t_begin);
-  } else {
-    t_begin = cta;
-    t_end = T;
-    t_count = static_cast<int>((T - cta + Gc - 1) / Gc);
   }
-  auto tile_of = [&](int i) -> long long {
-    if constexpr (C::CONTIG)
-      return t_begin + i;
-    else
-      return static_cast<long long>(cta) + static_cast<long long>(i) * Gc;
+  const long long ck = p.ck;
+  const long long chunk_t = static_cast<long long>(Gc) * ck;
+  const long long cbase = static_cast<long long>(cta) * ck;
+  const long long n_units = (!C::CONTIG && cbase < T) ? (T - cbase + chunk_t - 1) / chunk_t : 0;
+  auto unit_t0 = [&](long long j) { return j * chunk_t + cbase; };
+  auto unit_t1 = [&](long long j) { return (unit_t0(j) + ck < T) ? unit_t0(j) + ck : T; };
+  // producer / MMA: body(i, t), i = tile index in this CTA's sequence
+  auto walk_tiles = [&](auto&& body) {
+    int i = 0;
+    if constexpr (C::CONTIG) {
+      for (long long t = t_begin; t < t_end; ++t) body(i++, t);
+    } else {
+      for (long long j = 0; j < n_units; ++j)
+        for (long long t = unit_t0(j); t < unit_t1(j); ++t) body(i++, t);
+    }
+  };
+  // epilogue: body(i, it, t, pass, j, first_of_unit, last_of_unit); i counts
+  // epilogue items, it = the tile's index in the producer sequence (TMEM slot)
+  auto walk_epi = [&](auto&& body) {
+    int i = 0;
+    if constexpr (C::CONTIG) {
+      for (long long t = t_begin; t < t_end; ++t) {
+        body(i, i, t, 1, 0LL, t == t_begin, t == t_end - 1);
+        ++i;
+      }
+    } else {
+      const long long lag = p.lag;
+      for (long long q = 0; q < n_units + lag; ++q) {
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+          const long long j = pass ? q - lag : q;
+          if (j < 0 || j >= n_units) continue;
+          const long long t0 = unit_t0(j), t1 = unit_t1(j);
+          for (long long t = t0; t < t1; ++t)
+            body(i++, static_cast<int>(j * ck + (t - t0)), t, pass, j, t == t0, t == t1 - 1);
+        }
+      }
+    }
   };
 
   // ---- one-time setup
@@ -410,6 +544,10 @@ __global__ void __launch_bounds__(kThreads, (Cfg<OP, GR, MODE, OutT>::MINB))
     for (int a = 0; a < ACC; ++a) {
       ptx::mbar_init(&misc->tfull[a], 1);
       ptx::mbar_init(&misc->tempty[a], kEpiThreads);
+    }
+    for (int k = 0; k < 4; ++k) {
+      ptx::mbar_init(&misc->pfull[k], 1);
+      ptx::mbar_init(&misc->pempty[k], 4);  // one arrival per epilogue warp
     }
     misc->head_seg = -1;
     misc->head_val = 0.0;
@@ -429,22 +567,22 @@ __global__ void __launch_bounds__(kThreads, (Cfg<OP, GR, MODE, OutT>::MINB))
   if (warp == 0) {
     // ================= TMA producer =================
     if (lane == 0) {
-      const uint64_t pol = ptx::policy_evict_first();
-      for (int i = 0; i < t_count; ++i) {
+      const uint64_t pol = ptx::policy_evict_first();  // streamed exactly once
+      walk_tiles([&](int i, long long t) {
         const int s = i % STAGES;
         const uint32_t ph = (i / STAGES) & 1;
         ptx::mbar_wait(&misc->empty[s], ph ^ 1u);
         ptx::mbar_arrive_expect_tx(&misc->full[s], kTileBytes);
         ptx::tma_load_2d(&tin, smem + s * kTileBytes, &misc->full[s], 0,
-                         static_cast<int32_t>(tile_of(i) * kTileRows), pol);
-      }
+                         static_cast<int32_t>(t * kTileRows), pol);
+      });
     }
   } else if (warp == 1) {
     // ================= MMA issuer (one thread) =================
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_f16_f32(128, N);
       const uint64_t bdesc = ptx::smem_desc_sw128(smem + C::OFF_B);
-      for (int i = 0; i < t_count; ++i) {
+      walk_tiles([&](int i, long long) {
         const int s = i % STAGES;
         const uint32_t ph = (i / STAGES) & 1;
         const int a = i % ACC;
@@ -458,10 +596,10 @@ __global__ void __launch_bounds__(kThreads, (Cfg<OP, GR, MODE, OutT>::MINB))
           ptx::mma_f16_ss(tmem + a * N, adesc + 2 * k, bdesc + 2 * k, idesc, k > 0 ? 1u : 0u);
         ptx::mma_commit(&misc->empty[s]);
         ptx::mma_commit(&misc->tfull[a]);
-      }
+      });
     }
     __syncwarp();
-  } else {
+  } else if (warp < 6) {
     // ================= epilogue (warps 2..5) =================
     const int qd = warp & 3;          // TMEM lane quadrant
     const int rit = qd * 32 + lane;   // row in tile
@@ -474,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, (Cfg<OP, GR, MODE, OutT>::MINB))
 
     // running state
     double carry = 0.0;  // value of the segment open at the current tile's entry
-    long long q0 = (tile_of(0) * kTileRows + rit) * GR;  // first granule of this row
+    long long q0 = (t_begin * kTileRows + rit) * GR;     // first granule of this row
     long long qmod = 0, qdiv = 0;                        // GENERAL: q0 % m, q0 / m
     long long tpos = 0, tseg = 0;                        // TILES: t % k, t / k
     if constexpr (MODE == MODE_GENERAL) {
@@ -494,403 +632,676 @@ __global__ void __launch_bounds__(kThreads, (Cfg<OP, GR, MODE, OutT>::MINB))
       if (seg_start == 0 && has_carry) carry += *p.carry_in;
     }
 
-    for (int i = 0; i < t_count; ++i) {
-      const long long t = tile_of(i);
-      const int a = i % ACC;
-      const uint32_t aph = (i / ACC) & 1;
-      const int par = i & 1;
-      if constexpr (!C::CONTIG) {
-        q0 = (t * kTileRows + rit) * GR;
-      }
-      ptx::mbar_wait(&misc->tfull[a], aph);
-      ptx::tc_fence_after();
-      constexpr int LD = C::LD_COLS;
-      uint32_t r[LD];
-      if constexpr (LD <= 32) {
-        ptx::tmem_ld_32x32b<LD>(tmem + lane_base + a * N, r);
-      } else {
-        uint32_t(&r0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[0]);
-        uint32_t(&r1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[32]);
-        ptx::tmem_ld_32x32b<32>(tmem + lane_base + a * N, r0);
-        ptx::tmem_ld_32x32b<32>(tmem + lane_base + a * N + 32, r1);
-      }
-      ptx::tmem_wait_ld();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&misc->tempty[a]);
+    // CHUNK: aggregate of the unit being reduced (P1), and of the last two
+    // units, kept until their P2 (one-unit lag)
+    double u_v = 0.0;
+    int u_f = 0;
+    // CHUNK, one granule per row: does tile t hold a segment start?
+    // (rows < 2^31 since n < 2^37: 32-bit division, far cheaper than 64-bit)
+    auto tile_has_start = [&](long long t) -> bool {
+      const uint32_t r0 = static_cast<uint32_t>(t * kTileRows);
+      const uint32_t m32 = static_cast<uint32_t>(p.m);
+      long long fs = static_cast<long long>(r0 / m32) * m32;  // first start row >= r0
+      if (fs < r0) fs += m32;
+      if (fs == 0 && has_carry) fs = m32;  // row 0 continues the caller's segment
+      return fs < static_cast<long long>(r0) + kTileRows && fs <= p.qlast;
+    };
+    // hand the unit's aggregate to the prefix warp, which publishes it (the
+    // release store's fence would otherwise stall the TMA-issuing leader)
+    auto save_unit = [&](long long uj) {
+      if (leader) chunk_publish(p.u_word + uj * Gc + cta, u_v, u_f, ep);
+      u_v = 0.0;
+      u_f = 0;
+    };
 
-      const long long row = t * kTileRows + rit;
-
-      if constexpr (OP == OP_REDUCE) {
-        // ================================================= reduce
-        float gs[GR];
-#pragma unroll
-        for (int j = 0; j < GR; ++j) gs[j] = __uint_as_float(r[j]);
-        if (row == p.rows_full) {  // ragged last row: beyond the TMA view, patch from HBM
-          const long long e0 = row * kRow;
-#pragma unroll
-          for (int j = 0; j < GR; ++j) {
-            float s = 0.f;
-            for (int k = 0; k < G; ++k) {
-              const long long e = e0 + j * G + k;
-              if (e < p.n) s += __half2float(p.x[e]);
-            }
-            gs[j] = s;
+    if constexpr (OP == OP_SCAN && MODE == MODE_CHUNK && GR == 1) {
+      // ---- CHUNK with one granule (= one row) per segment step: fused
+      // steps.  Step s runs the A pass of tile s and the O pass of tile
+      // s - L*K of this CTA's sequence, sharing one TMEM wait and one
+      // cross-warp exchange barrier.  Tiles with a segment start use
+      // (value, flag) pair scans; all others plain row-total scans.
+      const long long lk = p.lag * ck;
+      const long long ntc =
+          n_units ? (n_units - 1) * ck + (unit_t1(n_units - 1) - unit_t0(n_units - 1)) : 0;
+      auto row_start = [&](long long row) -> int {
+        return (static_cast<uint32_t>(row) % static_cast<uint32_t>(p.m) == 0) && row <= p.qlast &&
+               !(row == 0 && has_carry);
+      };
+      long long ja = 0, ka = 0, jo = 0, ko = 0;  // (unit, tile-in-unit) of the A / O tiles
+      const bool excl = p.exclusive != 0;
+      double pacc = 0.0;  // this row's totals of start-free tiles not yet folded into u_v
+      double u_v = 0.0;   // unit aggregate so far (all threads hold the same value)
+      int u_f = 0;
+      int bpar = 0;       // exchange-buffer parity, flips once per exchange barrier
+      for (long long s2 = 0; s2 < ntc + lk; ++s2) {
+        const bool has_a = s2 < ntc;
+        const long long so = s2 - lk;
+        const bool has_o = so >= 0;
+        long long ta = 0, to = 0;
+        bool last_a = false, first_o = false, st_a = false, st_o = false;
+        const long long ja_c = ja, jo_c = jo;
+        if (has_a) {
+          ta = unit_t0(ja) + ka;
+          last_a = (ka == ck - 1) || (ta == T - 1);
+          st_a = tile_has_start(ta);
+          if (++ka == ck) {
+            ka = 0;
+            ++ja;
           }
         }
-        OutT* out = reinterpret_cast<OutT*>(p.out);
-        if constexpr (MODE == MODE_LOCAL) {
-          store_run<OutT, GR>(out, q0, gs, p.qlast);
-        } else if constexpr (MODE == MODE_ROWS) {
-          // segments = aligned groups of 2^log2m rows inside the tile
-          float v = gs[0];
-          const int msz = 1 << p.log2m;
-          if (msz <= 32) {
-            for (int d = 1; d < msz; d <<= 1) v += __shfl_xor_sync(kFull, v, d);
-            if ((lane & (msz - 1)) == 0) {
-              const long long sg = row >> p.log2m;
-              if (sg < p.nseg) out[sg] = cvt_out<OutT>(v);
+        if (has_o) {
+          to = unit_t0(jo) + ko;
+          first_o = (ko == 0);
+          st_o = tile_has_start(to);
+          if (++ko == ck) {
+            ko = 0;
+            ++jo;
+          }
+        }
+        // ---- TMEM: row total of tile A, full X.U row of tile O
+        const int sa = static_cast<int>(s2 & (ACC - 1));
+        const int sl_o = has_o ? static_cast<int>(so & (ACC - 1)) : 0;
+        uint32_t ra[1];
+        uint32_t ro[64];
+        if (has_a) ptx::mbar_wait_warp(&misc->tfull[sa], static_cast<uint32_t>((s2 >> 3) & 1));
+        static_assert(ACC == 8, "fused CHUNK epilogue assumes 8 TMEM tile slots");
+        ptx::tc_fence_after();
+        if (has_a) ptx::tmem_ld_32x32b<1>(tmem + lane_base + sa * N + 63, ra);
+        if (has_o) {
+          uint32_t(&r0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&ro[0]);
+          uint32_t(&r1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&ro[32]);
+          ptx::tmem_ld_32x32b<32>(tmem + lane_base + sl_o * N, r0);
+          ptx::tmem_ld_32x32b<32>(tmem + lane_base + sl_o * N + 32, r1);
+        }
+        ptx::tmem_wait_ld();
+        if (has_o) {
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&misc->tempty[sl_o]);
+        }
+        // ---- A part, warp level
+        const long long row_a = ta * kTileRows + rit;
+        float tot_a = __uint_as_float(ra[0]);
+        if (has_a && row_a == p.rows_full) {  // ragged last row: outside the TMA view
+          float acc = 0.f;
+#pragma unroll  // (a rolled loop here would keep ptxas from proving reconvergence)
+          for (int k = 0; k < kRow; ++k) {
+            const long long e = row_a * kRow + k;
+            if (e < p.n) acc += __half2float(p.x[e]);
+          }
+          tot_a = acc;
+        }
+        const bool bar_a = has_a && (st_a || last_a);
+        if (has_a && !st_a) pacc += static_cast<double>(tot_a);
+        __syncwarp();  // reconverge (ragged-row loop) so the shuffles below stay plain SHFL
+        if (bar_a) {
+          if (st_a) {
+            float v = tot_a;
+            int f = row_start(row_a);
+            warp_pair_scan(v, f, lane);
+            if (lane == 31) {
+              misc->pv[bpar][qd] = v;  // A tile pairs per warp
+              misc->pf[bpar][qd] = f;
+            }
+          }
+          const double pw = warp_sum_d(pacc);
+          if (lane == 0) misc->pd[bpar][qd] = pw;
+        }
+        // ---- O part, warp level
+        float vv[64];
+        const long long row_o = to * kTileRows + rit;
+        float o_ex = 0.f, o_ve = 0.f;
+        int o_fe = 0;
+        if (has_o) {
+#pragma unroll
+          for (int k = 0; k < 64; ++k) vv[k] = __uint_as_float(ro[k]);
+          if (row_o == p.rows_full) {  // ragged last row: recompute the row scan from HBM
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < 64; ++k) {
+              const long long e = row_o * kRow + k;
+              acc += (e < p.n) ? __half2float(p.x[e]) : 0.f;
+              vv[k] = acc;
+            }
+          }
+          if (leader) ptx::bulk_wait_read<C::OUT_BUFS - 1>();  // staging buffer free
+          __syncwarp();
+          const float tot = vv[63];
+          if (!st_o) {
+            const float incl = warp_incl_scan(tot, lane);
+            o_ex = __shfl_up_sync(kFull, incl, 1);
+            if (lane == 0) o_ex = 0.f;
+            if (lane == 31) misc->ov[bpar][qd] = incl;
+          } else {
+            float v = tot;
+            int f = row_start(row_o);
+            warp_pair_scan(v, f, lane);
+            o_ve = __shfl_up_sync(kFull, v, 1);
+            o_fe = __shfl_up_sync(kFull, f, 1);
+            if (lane == 0) {
+              o_ve = 0.f;
+              o_fe = 0;
+            }
+            if (lane == 31) {
+              misc->ov[bpar][qd] = v;
+              misc->of[bpar][qd] = f;
+            }
+          }
+        }
+        if (!bar_a && !has_o) continue;  // uniform: no exchange this step
+        ptx::named_bar_sync(kEpiBar, kEpiThreads);
+        // ---- A part, block level: fold into the unit; publish at its end
+        if (bar_a) {
+          u_v += ((misc->pd[bpar][0] + misc->pd[bpar][1]) + misc->pd[bpar][2]) +
+                 misc->pd[bpar][3];
+          pacc = 0.0;
+          if (st_a) {
+            float tv = 0.f;
+            int tf = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) compose(tv, tf, misc->pv[bpar][k], misc->pf[bpar][k]);
+            u_v = tf ? static_cast<double>(tv) : u_v + static_cast<double>(tv);
+            u_f |= tf;
+          }
+          if (last_a) {
+            if (leader) chunk_publish(p.u_word + ja_c * Gc + cta, u_v, u_f, ep);
+            u_v = 0.0;
+            u_f = 0;
+          }
+        }
+        if (has_o) {
+          // ---- O part, block level.  The entry value is awaited only now,
+          // after this step's A aggregate went out (keeps the L-unit slack).
+          if (first_o) {
+            const int ps = static_cast<int>(jo_c & 3);
+            ptx::mbar_wait_warp(&misc->pfull[ps], static_cast<uint32_t>((jo_c >> 2) & 1));
+            carry = misc->entry[ps];
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&misc->pempty[ps]);
+          }
+          float off;
+          if (!st_o) {
+            float woff = 0.f, ttot = 0.f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float y = misc->ov[bpar][k];
+              if (k < qd) woff += y;
+              ttot += y;
+            }
+            off = static_cast<float>(carry + static_cast<double>(o_ex + woff));
+            carry += static_cast<double>(ttot);
+          } else {
+            float wv = 0.f, tv = 0.f;
+            int wf = 0, tf = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float yv = misc->ov[bpar][k];
+              const int yf = misc->of[bpar][k];
+              if (k < qd) compose(wv, wf, yv, yf);
+              compose(tv, tf, yv, yf);
+            }
+            compose(wv, wf, o_ve, o_fe);
+            off = row_start(row_o) ? 0.f
+                                   : (wf ? wv : static_cast<float>(carry + static_cast<double>(wv)));
+            carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
+          }
+          auto outv = [&](int e) -> float {
+            if (excl) return (e == 0) ? (off + 0.f) : (vv[e - 1] + off);
+            return vv[e] + off;
+          };
+          if (p.total_out && row_o == (p.n - 1) / kRow) {
+            const int k = static_cast<int>((p.n - 1) % kRow);
+            float incl = 0.f;
+#pragma unroll
+            for (int e = 0; e < 64; ++e)
+              if (e == k) incl = vv[e] + off;
+            *p.total_out = static_cast<double>(incl);
+          }
+          uint8_t* stg = smem + C::OFF_OUT + (C::OUT_BUFS == 2 ? (so & 1) : 0) * C::OUT_BYTES;
+          const uint32_t rb = static_cast<uint32_t>(rit) * 128u;
+          const uint32_t sw = static_cast<uint32_t>(rit & 7);
+          if constexpr (sizeof(OutT) == 2) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              uint4 w;
+              __half2 h0 = __floats2half2_rn(outv(8 * c + 0), outv(8 * c + 1));
+              __half2 h1 = __floats2half2_rn(outv(8 * c + 2), outv(8 * c + 3));
+              __half2 h2 = __floats2half2_rn(outv(8 * c + 4), outv(8 * c + 5));
+              __half2 h3 = __floats2half2_rn(outv(8 * c + 6), outv(8 * c + 7));
+              w.x = *reinterpret_cast<uint32_t*>(&h0);
+              w.y = *reinterpret_cast<uint32_t*>(&h1);
+              w.z = *reinterpret_cast<uint32_t*>(&h2);
+              w.w = *reinterpret_cast<uint32_t*>(&h3);
+              *reinterpret_cast<uint4*>(stg + rb + ((c ^ sw) << 4)) = w;
             }
           } else {
-            v = warp_sum(v);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                float4 w = make_float4(outv(32 * h + 4 * c + 0), outv(32 * h + 4 * c + 1),
+                                       outv(32 * h + 4 * c + 2), outv(32 * h + 4 * c + 3));
+                *reinterpret_cast<float4*>(stg + h * 16384 + rb + ((c ^ sw) << 4)) = w;
+              }
+            }
+          }
+          if (row_o == p.rows_full) {  // ragged last row: direct stores
+            OutT* out = reinterpret_cast<OutT*>(p.out);
+#pragma unroll
+            for (int k = 0; k < 64; ++k) {
+              const long long e = row_o * kRow + k;
+              if (e < p.n) out[e] = cvt_out<OutT>(outv(k));
+            }
+          }
+          ptx::fence_proxy_async_smem();
+          ptx::named_bar_sync(kEpiBar, kEpiThreads);
+          if (leader) {
+            const int32_t r0 = static_cast<int32_t>(to * kTileRows);
+            ptx::tma_store_2d(&tout, stg, 0, r0);
+            if constexpr (sizeof(OutT) == 4) ptx::tma_store_2d(&tout, stg + 16384, 32, r0);
+            ptx::bulk_commit();
+          }
+        }
+        bpar ^= 1;
+      }
+    } else {
+      walk_epi([&](int i, int it, long long t, int pass, long long uj, bool first, bool last) {
+        // TMEM slot of the tile.  CHUNK: the A pass waits for the MMA, the O
+        // pass (a unit later) reads the same slot again and releases it.
+        const int a = it % ACC;
+        const uint32_t aph = (it / ACC) & 1;
+        const int par = i & 1;
+        const bool wait_full = C::CONTIG || pass == 0;
+        const bool release = C::CONTIG || pass == 1;
+        if constexpr (!C::CONTIG) {
+          q0 = (t * kTileRows + rit) * GR;
+        }
+        if (wait_full) ptx::mbar_wait_warp(&misc->tfull[a], aph);
+        ptx::tc_fence_after();
+        constexpr int LD = C::LD_COLS;
+        uint32_t r[LD];
+        if constexpr (LD <= 32) {
+          ptx::tmem_ld_32x32b<LD>(tmem + lane_base + a * N, r);
+        } else {
+          uint32_t(&r0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[0]);
+          uint32_t(&r1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[32]);
+          ptx::tmem_ld_32x32b<32>(tmem + lane_base + a * N, r0);
+          ptx::tmem_ld_32x32b<32>(tmem + lane_base + a * N + 32, r1);
+        }
+        ptx::tmem_wait_ld();
+        if (release) {
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&misc->tempty[a]);
+        }
+
+        const long long row = t * kTileRows + rit;
+
+        if constexpr (OP == OP_REDUCE) {
+          // ================================================= reduce
+          float gs[GR];
+  #pragma unroll
+          for (int j = 0; j < GR; ++j) gs[j] = __uint_as_float(r[j]);
+          if (row == p.rows_full) {  // ragged last row: beyond the TMA view, patch from HBM
+            const long long e0 = row * kRow;
+  #pragma unroll
+            for (int j = 0; j < GR; ++j) {
+              float s = 0.f;
+              for (int k = 0; k < G; ++k) {
+                const long long e = e0 + j * G + k;
+                if (e < p.n) s += __half2float(p.x[e]);
+              }
+              gs[j] = s;
+            }
+          }
+          OutT* out = reinterpret_cast<OutT*>(p.out);
+          if constexpr (MODE == MODE_LOCAL) {
+            store_run<OutT, GR>(out, q0, gs, p.qlast);
+          } else if constexpr (MODE == MODE_ROWS) {
+            // segments = aligned groups of 2^log2m rows inside the tile
+            float v = gs[0];
+            const int msz = 1 << p.log2m;
+            if (msz <= 32) {
+              for (int d = 1; d < msz; d <<= 1) v += __shfl_xor_sync(kFull, v, d);
+              if ((lane & (msz - 1)) == 0) {
+                const long long sg = row >> p.log2m;
+                if (sg < p.nseg) out[sg] = cvt_out<OutT>(v);
+              }
+            } else {
+              v = warp_sum(v);
+              if (lane == 0) misc->pv[par][qd] = v;
+              ptx::named_bar_sync(kEpiBar, kEpiThreads);
+              if (lane == 0) {
+                if (msz == 64 && (qd & 1) == 0) {
+                  const long long sg = row >> 6;
+                  if (sg < p.nseg)
+                    out[sg] = cvt_out<OutT>(misc->pv[par][qd] + misc->pv[par][qd + 1]);
+                } else if (msz == 128 && qd == 0) {
+                  const float s4 = (misc->pv[par][0] + misc->pv[par][1]) +
+                                   (misc->pv[par][2] + misc->pv[par][3]);
+                  out[t] = cvt_out<OutT>(s4);
+                }
+              }
+            }
+          } else if constexpr (MODE == MODE_TILES) {
+            // whole tiles belong to one segment of ktiles tiles
+            const float v = warp_sum(gs[0]);
             if (lane == 0) misc->pv[par][qd] = v;
             ptx::named_bar_sync(kEpiBar, kEpiThreads);
-            if (lane == 0) {
-              if (msz == 64 && (qd & 1) == 0) {
-                const long long sg = row >> 6;
-                if (sg < p.nseg)
-                  out[sg] = cvt_out<OutT>(misc->pv[par][qd] + misc->pv[par][qd + 1]);
-              } else if (msz == 128 && qd == 0) {
-                const float s4 = (misc->pv[par][0] + misc->pv[par][1]) +
-                                 (misc->pv[par][2] + misc->pv[par][3]);
-                out[t] = cvt_out<OutT>(s4);
-              }
-            }
-          }
-        } else if constexpr (MODE == MODE_TILES) {
-          // whole tiles belong to one segment of ktiles tiles
-          const float v = warp_sum(gs[0]);
-          if (lane == 0) misc->pv[par][qd] = v;
-          ptx::named_bar_sync(kEpiBar, kEpiThreads);
-          const float tsum = (misc->pv[par][0] + misc->pv[par][1]) +
-                             (misc->pv[par][2] + misc->pv[par][3]);
-          if (tpos == 0) carry = 0.0;
-          carry += static_cast<double>(tsum);
-          if ((tpos == p.ktiles - 1 || t == T - 1) && leader) {
-            if (tseg * p.seg < range_first_elem) {
-              misc->head_seg = tseg;  // began in an earlier CTA's range
-              misc->head_val = carry;
-            } else {
-              out[tseg] = cvt_out_d<OutT>(carry);
-            }
-          }
-          if (++tpos == p.ktiles) {
-            tpos = 0;
-            ++tseg;
-          }
-        } else {
-          // MODE_GENERAL: segmented (value, has_end) pair scan over rows
-          long long rem = p.m - 1 - qmod;  // granules until the next segment end
-          long long sg = qdiv;             // segment containing granule q0 + j
-          const long long seg0 = sg;       // segment closed by the row's first end
-          float run = 0.f, head = 0.f;
-          int seen = 0;
-#pragma unroll
-          for (int j = 0; j < GR; ++j) {
-            run += gs[j];
-            const long long qj = q0 + j;
-            if (qj <= p.qlast && (rem == 0 || qj == p.qlast)) {
-              if (!seen) {
-                head = run;  // needs the carry from earlier rows / tiles
-                seen = 1;
+            const float tsum = (misc->pv[par][0] + misc->pv[par][1]) +
+                               (misc->pv[par][2] + misc->pv[par][3]);
+            if (tpos == 0) carry = 0.0;
+            carry += static_cast<double>(tsum);
+            if ((tpos == p.ktiles - 1 || t == T - 1) && leader) {
+              if (tseg * p.seg < range_first_elem) {
+                misc->head_seg = tseg;  // began in an earlier CTA's range
+                misc->head_val = carry;
               } else {
-                out[sg] = cvt_out<OutT>(run);  // segment wholly inside this row
+                out[tseg] = cvt_out_d<OutT>(carry);
               }
-              ++sg;
-              run = 0.f;
             }
-            rem = (rem == 0) ? p.m - 1 : rem - 1;
-          }
-          float v = run;
-          int f = seen;
-          warp_pair_scan(v, f, lane);
-          float ve = __shfl_up_sync(kFull, v, 1);
-          int fe = __shfl_up_sync(kFull, f, 1);
-          if (lane == 0) {
-            ve = 0.f;
-            fe = 0;
-          }
-          if (lane == 31) {
-            misc->pv[par][qd] = v;
-            misc->pf[par][qd] = f;
-          }
-          ptx::named_bar_sync(kEpiBar, kEpiThreads);
-          float wv = 0.f, tv = 0.f;
-          int wf = 0, tf = 0;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float yv = misc->pv[par][k];
-            const int yf = misc->pf[par][k];
-            if (k < qd) compose(wv, wf, yv, yf);
-            compose(tv, tf, yv, yf);
-          }
-          compose(wv, wf, ve, fe);
-          if (seen) {
-            const double val = static_cast<double>(wv + head) + (wf ? 0.0 : carry);
-            if (seg0 * p.seg < range_first_elem) {
-              misc->head_seg = seg0;  // partial: segment began in an earlier CTA's range
-              misc->head_val = val;
-            } else {
-              out[seg0] = cvt_out_d<OutT>(val);
+            if (++tpos == p.ktiles) {
+              tpos = 0;
+              ++tseg;
             }
-          }
-          carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
-          // advance to the next tile's row (contiguous ranges)
-          qmod += p.step_mod;
-          qdiv += p.step_div;
-          if (qmod >= p.m) {
-            qmod -= p.m;
-            ++qdiv;
-          }
-        }
-        q0 += static_cast<long long>(kTileRows) * GR;
-      } else {
-        // ================================================= scan
-        float vv[64];
-#pragma unroll
-        for (int k = 0; k < 64; ++k) vv[k] = __uint_as_float(r[k]);
-        if (row == p.rows_full) {  // ragged last row: recompute in-granule scans from HBM
-          const long long e0 = row * kRow;
-          float s = 0.f;
-#pragma unroll
-          for (int k = 0; k < 64; ++k) {
-            if (k % G == 0) s = 0.f;
-            const long long e = e0 + k;
-            s += (e < p.n) ? __half2float(p.x[e]) : 0.f;
-            vv[k] = s;
-          }
-        }
-        // staging buffer reuse: the TMA store that last used this buffer
-        // must have finished reading it before anyone writes (barrier below).
-        if (leader) ptx::bulk_wait_read<C::OUT_BUFS - 1>();
-        float off[GR];  // per-granule offset to add (exclusive prefix within segment)
-        if constexpr (MODE == MODE_LOCAL) {
-          ptx::named_bar_sync(kEpiBar, kEpiThreads);
-#pragma unroll
-          for (int j = 0; j < GR; ++j) off[j] = 0.f;
-        } else if constexpr (MODE == MODE_ROWS) {
-          const float tot = vv[63];
-          const int msz = 1 << p.log2m;
-          float incl = tot;
-          float excl;
-          if (msz <= 32) {
-            const int pos = lane & (msz - 1);
-            for (int d = 1; d < msz; d <<= 1) {
-              const float u = __shfl_up_sync(kFull, incl, d);
-              if (pos >= d) incl += u;
-            }
-            excl = __shfl_up_sync(kFull, incl, 1);
-            if (pos == 0) excl = 0.f;
-            ptx::named_bar_sync(kEpiBar, kEpiThreads);
           } else {
-            incl = warp_incl_scan(incl, lane);
-            excl = __shfl_up_sync(kFull, incl, 1);
-            if (lane == 0) excl = 0.f;
-            if (lane == 31) misc->pv[par][qd] = incl;
-            ptx::named_bar_sync(kEpiBar, kEpiThreads);
-            float woff = 0.f;
-            if (msz == 64) {
-              if (qd & 1) woff = misc->pv[par][qd - 1];
-            } else {
-#pragma unroll
-              for (int k = 0; k < 3; ++k)
-                if (k < qd) woff += misc->pv[par][k];
-            }
-            excl += woff;
-          }
-          off[0] = excl;
-        } else if constexpr (MODE == MODE_TILES) {
-          const float tot = vv[63];
-          float incl = warp_incl_scan(tot, lane);
-          float excl = __shfl_up_sync(kFull, incl, 1);
-          if (lane == 0) excl = 0.f;
-          if (lane == 31) misc->pv[par][qd] = incl;
-          ptx::named_bar_sync(kEpiBar, kEpiThreads);
-          float woff = 0.f, ttot = 0.f;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float y = misc->pv[par][k];
-            if (k < qd) woff += y;
-            ttot += y;
-          }
-          if (tpos == 0) carry = 0.0;  // a segment starts at this tile
-          off[0] = static_cast<float>(carry + static_cast<double>(excl + woff));
-          carry += static_cast<double>(ttot);
-          if (++tpos == p.ktiles) {
-            tpos = 0;
-            ++tseg;
-          }
-        } else {
-          // MODE_GENERAL / MODE_LOOKBACK: pair scan with granule starts
-          int chain[GR];
-          float run = 0.f;
-          int seen = 0;
-          {
-            long long qm = (MODE == MODE_GENERAL) ? qmod : (q0 % p.m);
-            long long rem = qm == 0 ? 0 : p.m - qm;  // granules until the next start
-#pragma unroll
+            // MODE_GENERAL: segmented (value, has_end) pair scan over rows
+            long long rem = p.m - 1 - qmod;  // granules until the next segment end
+            long long sg = qdiv;             // segment containing granule q0 + j
+            const long long seg0 = sg;       // segment closed by the row's first end
+            float run = 0.f, head = 0.f;
+            int seen = 0;
+  #pragma unroll
             for (int j = 0; j < GR; ++j) {
-              const bool st =
-                  (rem == 0) && (q0 + j <= p.qlast) && !((q0 + j) == 0 && has_carry);
-              if (st) {
+              run += gs[j];
+              const long long qj = q0 + j;
+              if (qj <= p.qlast && (rem == 0 || qj == p.qlast)) {
+                if (!seen) {
+                  head = run;  // needs the carry from earlier rows / tiles
+                  seen = 1;
+                } else {
+                  out[sg] = cvt_out<OutT>(run);  // segment wholly inside this row
+                }
+                ++sg;
                 run = 0.f;
-                seen = 1;
               }
-              off[j] = run;
-              chain[j] = !seen;
-              run += vv[j * G + G - 1];
               rem = (rem == 0) ? p.m - 1 : rem - 1;
             }
-          }
-          float v = run;
-          int f = seen;
-          warp_pair_scan(v, f, lane);
-          float ve = __shfl_up_sync(kFull, v, 1);
-          int fe = __shfl_up_sync(kFull, f, 1);
-          if (lane == 0) {
-            ve = 0.f;
-            fe = 0;
-          }
-          if (lane == 31) {
-            misc->pv[par][qd] = v;
-            misc->pf[par][qd] = f;
-          }
-          ptx::named_bar_sync(kEpiBar, kEpiThreads);
-          float wv = 0.f, tv = 0.f;
-          int wf = 0, tf = 0;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float yv = misc->pv[par][k];
-            const int yf = misc->pf[par][k];
-            if (k < qd) compose(wv, wf, yv, yf);
-            compose(tv, tf, yv, yf);
-          }
-          compose(wv, wf, ve, fe);
-          double tprefix;
-          if constexpr (MODE == MODE_GENERAL) {
-            tprefix = carry;
+            float v = run;
+            int f = seen;
+            warp_pair_scan(v, f, lane);
+            float ve = __shfl_up_sync(kFull, v, 1);
+            int fe = __shfl_up_sync(kFull, f, 1);
+            if (lane == 0) {
+              ve = 0.f;
+              fe = 0;
+            }
+            if (lane == 31) {
+              misc->pv[par][qd] = v;
+              misc->pf[par][qd] = f;
+            }
+            ptx::named_bar_sync(kEpiBar, kEpiThreads);
+            float wv = 0.f, tv = 0.f;
+            int wf = 0, tf = 0;
+  #pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float yv = misc->pv[par][k];
+              const int yf = misc->pf[par][k];
+              if (k < qd) compose(wv, wf, yv, yf);
+              compose(tv, tf, yv, yf);
+            }
+            compose(wv, wf, ve, fe);
+            if (seen) {
+              const double val = static_cast<double>(wv + head) + (wf ? 0.0 : carry);
+              if (seg0 * p.seg < range_first_elem) {
+                misc->head_seg = seg0;  // partial: segment began in an earlier CTA's range
+                misc->head_val = val;
+              } else {
+                out[seg0] = cvt_out_d<OutT>(val);
+              }
+            }
             carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
+            // advance to the next tile's row (contiguous ranges)
             qmod += p.step_mod;
             qdiv += p.step_div;
             if (qmod >= p.m) {
               qmod -= p.m;
               ++qdiv;
             }
+          }
+          q0 += static_cast<long long>(kTileRows) * GR;
+        } else {
+          // ================================================= scan
+          float vv[64];
+  #pragma unroll
+          for (int k = 0; k < 64; ++k) vv[k] = __uint_as_float(r[k]);
+          if (row == p.rows_full) {  // ragged last row: recompute in-granule scans from HBM
+            const long long e0 = row * kRow;
+            float s = 0.f;
+  #pragma unroll
+            for (int k = 0; k < 64; ++k) {
+              if (k % G == 0) s = 0.f;
+              const long long e = e0 + k;
+              s += (e < p.n) ? __half2float(p.x[e]) : 0.f;
+              vv[k] = s;
+            }
+          }
+          // staging buffer reuse: the TMA store that last used this buffer
+          // must have finished reading it before anyone writes (barrier below).
+          if (leader) ptx::bulk_wait_read<C::OUT_BUFS - 1>();
+          float off[GR];  // per-granule offset to add (exclusive prefix within segment)
+          if constexpr (MODE == MODE_LOCAL) {
+            ptx::named_bar_sync(kEpiBar, kEpiThreads);
+  #pragma unroll
+            for (int j = 0; j < GR; ++j) off[j] = 0.f;
+          } else if constexpr (MODE == MODE_ROWS) {
+            const float tot = vv[63];
+            const int msz = 1 << p.log2m;
+            float incl = tot;
+            float excl;
+            if (msz <= 32) {
+              const int pos = lane & (msz - 1);
+              for (int d = 1; d < msz; d <<= 1) {
+                const float u = __shfl_up_sync(kFull, incl, d);
+                if (pos >= d) incl += u;
+              }
+              excl = __shfl_up_sync(kFull, incl, 1);
+              if (pos == 0) excl = 0.f;
+              ptx::named_bar_sync(kEpiBar, kEpiThreads);
+            } else {
+              incl = warp_incl_scan(incl, lane);
+              excl = __shfl_up_sync(kFull, incl, 1);
+              if (lane == 0) excl = 0.f;
+              if (lane == 31) misc->pv[par][qd] = incl;
+              ptx::named_bar_sync(kEpiBar, kEpiThreads);
+              float woff = 0.f;
+              if (msz == 64) {
+                if (qd & 1) woff = misc->pv[par][qd - 1];
+              } else {
+  #pragma unroll
+                for (int k = 0; k < 3; ++k)
+                  if (k < qd) woff += misc->pv[par][k];
+              }
+              excl += woff;
+            }
+            off[0] = excl;
+          } else if constexpr (MODE == MODE_TILES) {
+            const float tot = vv[63];
+            float incl = warp_incl_scan(tot, lane);
+            float excl = __shfl_up_sync(kFull, incl, 1);
+            if (lane == 0) excl = 0.f;
+            if (lane == 31) misc->pv[par][qd] = incl;
+            ptx::named_bar_sync(kEpiBar, kEpiThreads);
+            float woff = 0.f, ttot = 0.f;
+  #pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float y = misc->pv[par][k];
+              if (k < qd) woff += y;
+              ttot += y;
+            }
+            if (tpos == 0) carry = 0.0;  // a segment starts at this tile
+            off[0] = static_cast<float>(carry + static_cast<double>(excl + woff));
+            carry += static_cast<double>(ttot);
+            if (++tpos == p.ktiles) {
+              tpos = 0;
+              ++tseg;
+            }
           } else {
-            // decoupled look-back across tiles (huge segments)
-            const long long tq0 = t * static_cast<long long>(kTileRows) * GR;
-            const bool first_start = (tq0 % p.m == 0) && !(t == 0 && has_carry);
-            if (warp == 2) {
-              if (lane == 0) {
-                if (tf)
-                  publish(p, t, ep, 2, static_cast<double>(tv));
-                else if (!(t == 0 || first_start))
-                  publish(p, t, ep, 1, static_cast<double>(tv));
+            // MODE_GENERAL / MODE_CHUNK: pair scan with granule starts
+            if constexpr (MODE == MODE_CHUNK) {
+              if (pass == 1 && first) {
+                // value entering the unit, composed by the prefix warp
+                const int ps = static_cast<int>(uj & 3);
+                ptx::mbar_wait_warp(&misc->pfull[ps], static_cast<uint32_t>((uj >> 2) & 1));
+                carry = misc->entry[ps];
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&misc->pempty[ps]);
               }
-              double pre;
-              if (t == 0)
-                pre = has_carry ? *p.carry_in : 0.0;
-              else if (first_start)
-                pre = 0.0;
-              else
-                pre = lookback(p, t, ep, lane);
-              if (lane == 0) {
-                const double incl = tf ? static_cast<double>(tv) : pre + static_cast<double>(tv);
-                if (!tf) publish(p, t, ep, 2, incl);
-                misc->lb_prefix[par] = pre;
+            }
+            int chain[GR];
+            float run = 0.f;
+            int seen = 0;
+            {
+              const long long qm = (MODE == MODE_GENERAL) ? qmod : (q0 % p.m);
+              long long rem = qm == 0 ? 0 : p.m - qm;  // granules until the next start
+  #pragma unroll
+              for (int j = 0; j < GR; ++j) {
+                const bool st =
+                    (rem == 0) && (q0 + j <= p.qlast) && !((q0 + j) == 0 && has_carry);
+                if (st) {
+                  run = 0.f;
+                  seen = 1;
+                }
+                off[j] = run;
+                chain[j] = !seen;
+                run += vv[j * G + G - 1];
+                rem = (rem == 0) ? p.m - 1 : rem - 1;
               }
+            }
+            float v = run;
+            int f = seen;
+            warp_pair_scan(v, f, lane);
+            float ve = __shfl_up_sync(kFull, v, 1);
+            int fe = __shfl_up_sync(kFull, f, 1);
+            if (lane == 0) {
+              ve = 0.f;
+              fe = 0;
+            }
+            if (lane == 31) {
+              misc->pv[par][qd] = v;
+              misc->pf[par][qd] = f;
             }
             ptx::named_bar_sync(kEpiBar, kEpiThreads);
-            tprefix = misc->lb_prefix[par];
+            float wv = 0.f, tv = 0.f;
+            int wf = 0, tf = 0;
+  #pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float yv = misc->pv[par][k];
+              const int yf = misc->pf[par][k];
+              if (k < qd) compose(wv, wf, yv, yf);
+              compose(tv, tf, yv, yf);
+            }
+            compose(wv, wf, ve, fe);
+            double tprefix;
+            if constexpr (MODE == MODE_GENERAL) {
+              tprefix = carry;
+              carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
+              qmod += p.step_mod;
+              qdiv += p.step_div;
+              if (qmod >= p.m) {
+                qmod -= p.m;
+                ++qdiv;
+              }
+            } else {
+              // MODE_CHUNK
+              if (pass == 0) {
+                // P1: fold the tile aggregate into the unit's; publish at the unit's end
+                u_v = tf ? static_cast<double>(tv) : u_v + static_cast<double>(tv);
+                u_f |= tf;
+                if (last) save_unit(uj);
+                return;  // no output in the reduce pass
+              }
+              tprefix = carry;
+              carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
+            }
+            const float cinf = wf ? wv : static_cast<float>(tprefix + static_cast<double>(wv));
+  #pragma unroll
+            for (int j = 0; j < GR; ++j)
+              if (chain[j]) off[j] += cinf;
           }
-          const float cinf = wf ? wv : static_cast<float>(tprefix + static_cast<double>(wv));
-#pragma unroll
-          for (int j = 0; j < GR; ++j)
-            if (chain[j]) off[j] += cinf;
-        }
-        // outputs: in-granule scan + granule offset (exclusive: shifted),
-        // produced chunk by chunk straight into the swizzled staging tile.
-        constexpr bool ONE_OFF = (MODE == MODE_ROWS || MODE == MODE_TILES);
-        const bool excl = p.exclusive != 0;
-        auto outv = [&](int e) -> float {
-          const float base = off[ONE_OFF ? 0 : e / G];
-          if (excl) return (e % G == 0) ? (base + 0.f) : (vv[e - 1] + base);
-          return vv[e] + base;
-        };
-        if (p.total_out && row == (p.n - 1) / kRow) {
-          const int k = static_cast<int>((p.n - 1) % kRow);
-          float incl = 0.f;
-#pragma unroll
-          for (int e = 0; e < 64; ++e)
-            if (e == k) incl = vv[e] + off[ONE_OFF ? 0 : e / G];
-          *p.total_out = static_cast<double>(incl);
-        }
-        uint8_t* stg = smem + C::OFF_OUT + (C::OUT_BUFS == 2 ? par : 0) * C::OUT_BYTES;
-        const uint32_t rb = static_cast<uint32_t>(rit) * 128u;
-        const uint32_t sw = static_cast<uint32_t>(rit & 7);
-        if constexpr (sizeof(OutT) == 2) {
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            uint4 w;
-            __half2 h0 = __floats2half2_rn(outv(8 * c + 0), outv(8 * c + 1));
-            __half2 h1 = __floats2half2_rn(outv(8 * c + 2), outv(8 * c + 3));
-            __half2 h2 = __floats2half2_rn(outv(8 * c + 4), outv(8 * c + 5));
-            __half2 h3 = __floats2half2_rn(outv(8 * c + 6), outv(8 * c + 7));
-            w.x = *reinterpret_cast<uint32_t*>(&h0);
-            w.y = *reinterpret_cast<uint32_t*>(&h1);
-            w.z = *reinterpret_cast<uint32_t*>(&h2);
-            w.w = *reinterpret_cast<uint32_t*>(&h3);
-            *reinterpret_cast<uint4*>(stg + rb + ((c ^ sw) << 4)) = w;
+          // outputs: in-granule scan + granule offset (exclusive: shifted),
+          // produced chunk by chunk straight into the swizzled staging tile.
+          constexpr bool ONE_OFF = (MODE == MODE_ROWS || MODE == MODE_TILES);
+          const bool excl = p.exclusive != 0;
+          auto outv = [&](int e) -> float {
+            const float base = off[ONE_OFF ? 0 : e / G];
+            if (excl) return (e % G == 0) ? (base + 0.f) : (vv[e - 1] + base);
+            return vv[e] + base;
+          };
+          if (p.total_out && row == (p.n - 1) / kRow) {
+            const int k = static_cast<int>((p.n - 1) % kRow);
+            float incl = 0.f;
+  #pragma unroll
+            for (int e = 0; e < 64; ++e)
+              if (e == k) incl = vv[e] + off[ONE_OFF ? 0 : e / G];
+            *p.total_out = static_cast<double>(incl);
           }
-        } else {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-#pragma unroll
+          uint8_t* stg = smem + C::OFF_OUT + (C::OUT_BUFS == 2 ? par : 0) * C::OUT_BYTES;
+          const uint32_t rb = static_cast<uint32_t>(rit) * 128u;
+          const uint32_t sw = static_cast<uint32_t>(rit & 7);
+          if constexpr (sizeof(OutT) == 2) {
+  #pragma unroll
             for (int c = 0; c < 8; ++c) {
-              float4 w = make_float4(outv(32 * h + 4 * c + 0), outv(32 * h + 4 * c + 1),
-                                     outv(32 * h + 4 * c + 2), outv(32 * h + 4 * c + 3));
-              *reinterpret_cast<float4*>(stg + h * 16384 + rb + ((c ^ sw) << 4)) = w;
+              uint4 w;
+              __half2 h0 = __floats2half2_rn(outv(8 * c + 0), outv(8 * c + 1));
+              __half2 h1 = __floats2half2_rn(outv(8 * c + 2), outv(8 * c + 3));
+              __half2 h2 = __floats2half2_rn(outv(8 * c + 4), outv(8 * c + 5));
+              __half2 h3 = __floats2half2_rn(outv(8 * c + 6), outv(8 * c + 7));
+              w.x = *reinterpret_cast<uint32_t*>(&h0);
+              w.y = *reinterpret_cast<uint32_t*>(&h1);
+              w.z = *reinterpret_cast<uint32_t*>(&h2);
+              w.w = *reinterpret_cast<uint32_t*>(&h3);
+              *reinterpret_cast<uint4*>(stg + rb + ((c ^ sw) << 4)) = w;
+            }
+          } else {
+  #pragma unroll
+            for (int h = 0; h < 2; ++h) {
+  #pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                float4 w = make_float4(outv(32 * h + 4 * c + 0), outv(32 * h + 4 * c + 1),
+                                       outv(32 * h + 4 * c + 2), outv(32 * h + 4 * c + 3));
+                *reinterpret_cast<float4*>(stg + h * 16384 + rb + ((c ^ sw) << 4)) = w;
+              }
             }
           }
-        }
-        if (row == p.rows_full) {  // ragged last row is outside the TMA view: direct stores
-          OutT* out = reinterpret_cast<OutT*>(p.out);
-#pragma unroll
-          for (int k = 0; k < 64; ++k) {
-            const long long e = row * kRow + k;
-            if (e < p.n) out[e] = cvt_out<OutT>(outv(k));
+          if (row == p.rows_full) {  // ragged last row is outside the TMA view: direct stores
+            OutT* out = reinterpret_cast<OutT*>(p.out);
+  #pragma unroll
+            for (int k = 0; k < 64; ++k) {
+              const long long e = row * kRow + k;
+              if (e < p.n) out[e] = cvt_out<OutT>(outv(k));
+            }
           }
-        }
-        ptx::fence_proxy_async_smem();
-        ptx::named_bar_sync(kEpiBar, kEpiThreads);
-        if (leader) {
-          const int32_t r0 = static_cast<int32_t>(t * kTileRows);
-          if constexpr (sizeof(OutT) == 2) {
-            ptx::tma_store_2d(&tout, stg, 0, r0);
-          } else {
-            ptx::tma_store_2d(&tout, stg, 0, r0);
-            ptx::tma_store_2d(&tout, stg + 16384, 32, r0);
+          ptx::fence_proxy_async_smem();
+          ptx::named_bar_sync(kEpiBar, kEpiThreads);
+          if (leader) {
+            const int32_t r0 = static_cast<int32_t>(t * kTileRows);
+            if constexpr (sizeof(OutT) == 2) {
+              ptx::tma_store_2d(&tout, stg, 0, r0);
+            } else {
+              ptx::tma_store_2d(&tout, stg, 0, r0);
+              ptx::tma_store_2d(&tout, stg + 16384, 32, r0);
+            }
+            ptx::bulk_commit();
           }
-          ptx::bulk_commit();
+          q0 += static_cast<long long>(kTileRows) * GR;
         }
-        q0 += static_cast<long long>(kTileRows) * GR;
-      }
-    }  // tile loop
+      });  // tile loop
+    }
 
     if constexpr (OP == OP_SCAN) {
       if (leader) ptx::bulk_wait<0>();
     }
     // ---- cross-CTA completion: reduce partial fixup / look-back epoch bump
-    const bool need_ticket = (OP == OP_REDUCE) ? (p.need_fixup != 0) : (MODE == MODE_LOOKBACK);
+    const bool need_ticket = (OP == OP_REDUCE) ? (p.need_fixup != 0) : (MODE == MODE_CHUNK);
     if (need_ticket) {
       ptx::named_bar_sync(kEpiBar, kEpiThreads);
       if (leader) {
@@ -949,6 +1360,11 @@ __global__ void __launch_bounds__(kThreads, (Cfg<OP, GR, MODE, OutT>::MINB))
         }
       }
     }
+  } else {
+    // ================= prefix warp (CHUNK only) =================
+    if constexpr (MODE == MODE_CHUNK)
+      prefix_warp(p, misc, n_units, cta, Gc, ck, T, lane, (p.hdr->epoch + 1u) & 0x3FFFFFFFu,
+                  p.carry_in != nullptr);
   }
 
   // ---- teardown
@@ -1030,14 +1446,42 @@ static long long gcd_ll(long long a, long long b) {
   return a;
 }
 
+// CHUNK arrays: units u = j*Gc + c < T + kMaxCtas, chunks j < T
+static long long chunk_slots(long long n) { return (n + kTileElems - 1) / kTileElems + kMaxCtas; }
+
 static size_t ws_need(int op, long long n, long long seg) {
   (void)seg;
   size_t b = kWsLookback;
-  if (op == TC_OP_SCAN) {
-    const long long T = (n + kTileElems - 1) / kTileElems;
-    b += static_cast<size_t>(T) * (sizeof(uint32_t) + 2 * sizeof(double)) + 64;
-  }
+  if (op == TC_OP_SCAN)
+    b += static_cast<size_t>(chunk_slots(n)) * sizeof(uint64_t) + 64;
   return (b + 255) & ~size_t(255);
+}
+
+// CHUNK unit size: K tiles per CTA per chunk.  A unit's tiles stay in TMEM
+// from its A pass to its O pass, one unit later, so two units must fit the
+// 8 TMEM tile slots: K <= 4 (K = 2 leaves a third unit for the MMA to fill
+// meanwhile).  TC_CHUNK_TILES overrides (tuning).
+static long long chunk_tiles(long long T, long long grid) {
+  const char* e = getenv("TC_CHUNK_TILES");
+  long long k = (e && atoll(e) > 0) ? atoll(e) : 2;
+  if (k > 4) k = 4;
+  const long long fair = T / (grid > 0 ? grid : 1);
+  if (k > fair) k = fair;
+  return k < 1 ? 1 : k;
+}
+
+// CHUNK lag L: O(j) runs after A(j+L), so the cross-CTA wait for unit j's
+// entry value has L units of slack.  Units j..j+L must all be resident in
+// the 8 TMEM tile slots, (L + 1) * K <= 8 (else A(j+L) would wait for a slot
+// only O(j) frees: deadlock).  Measured on B200 (2^30, fp32 out): K = 2,
+// L = 3 is best; L = 1 leaves the ~5 us publish-to-observe latency under
+// full HBM load exposed.
+static long long chunk_lag(long long k) {
+  const long long lmax = 8 / k - 1;
+  const char* e = getenv("TC_CHUNK_LAG");
+  long long l = (e && atoll(e) > 0) ? atoll(e) : lmax;
+  if (l > lmax) l = lmax;
+  return l < 1 ? 1 : l;
 }
 
 template <int OP, int GR, int MODE, typename OutT>
@@ -1062,7 +1506,7 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
     return TC_NO_DEVICE;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg<OP, GR, MODE, OutT>::THREADS, smem) !=
           cudaSuccess ||
       per_sm < 1) {
     set_err("occupancy query failed: %s%lld", cudaGetErrorString(cudaGetLastError()), 0);
@@ -1072,9 +1516,14 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
   long long grid = static_cast<long long>(di.sms) * per_sm;
   if (grid > p0.num_tiles) grid = p0.num_tiles;
   if (grid > kMaxCtas) grid = kMaxCtas;
+  if (MODE == MODE_CHUNK && grid > 256) grid = 256;  // prefix warp reads <= 8 units per lane
   if (grid < 1) grid = 1;
 
-  const Params& p = p0;
+  Params p = p0;
+  if (MODE == MODE_CHUNK) {
+    p.ck = chunk_tiles(p.num_tiles, grid);
+    p.lag = chunk_lag(p.ck);
+  }
   CUtensorMap tin, tout;
   const char* wsb = reinterpret_cast<const char*>(p.hdr);
   const void* in_base = p.rows_full > 0 ? static_cast<const void*>(p.x)
@@ -1100,13 +1549,13 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(Cfg<OP, GR, MODE, OutT>::THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   int na = 0;
-  if (MODE == MODE_LOOKBACK) {
-    // decoupled look-back needs every CTA resident: cooperative launch
+  if (MODE == MODE_CHUNK) {
+    // the cross-CTA spin-waits need every CTA resident: cooperative launch
     // guarantees co-residency (or fails loudly instead of deadlocking).
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
@@ -1146,8 +1595,8 @@ static LaunchFn pick(int gr, int mode) {
     case MODE_ROWS: return gr == 1 ? &launch<OP, 1, MODE_ROWS, OutT> : nullptr;
     case MODE_TILES: return gr == 1 ? &launch<OP, 1, MODE_TILES, OutT> : nullptr;
     case MODE_GENERAL: return pick_gr<OP, MODE_GENERAL, OutT>(gr);
-    case MODE_LOOKBACK:
-      if constexpr (OP == OP_SCAN) return pick_gr<OP, MODE_LOOKBACK, OutT>(gr);
+    case MODE_CHUNK:
+      if constexpr (OP == OP_SCAN) return pick_gr<OP, MODE_CHUNK, OutT>(gr);
       return nullptr;
   }
   return nullptr;
@@ -1220,18 +1669,16 @@ static Params make_params(const void* x, long long n, long long seg, void* out, 
   }
   if (op == TC_OP_SCAN && (mode == MODE_TILES || mode == MODE_GENERAL) &&
       (seg > kScanPrepassMax || scan_carry))
-    mode = MODE_LOOKBACK;
+    mode = MODE_CHUNK;
   *gr_out = gr;
   *mode_out = mode;
   char* w = reinterpret_cast<char*>(ws);
   p.hdr = reinterpret_cast<WsHeader*>(w);
   p.entries = reinterpret_cast<Entry*>(w + kWsEntries);
-  const long long T = p.num_tiles;
-  p.lb_flag = reinterpret_cast<uint32_t*>(w + kWsLookback);
-  size_t off = kWsLookback + ((static_cast<size_t>(T) * 4 + 15) & ~size_t(15));
-  p.lb_agg = reinterpret_cast<double*>(w + off);
-  off += static_cast<size_t>(T) * 8;
-  p.lb_inc = reinterpret_cast<double*>(w + off);
+  const size_t slots = static_cast<size_t>(chunk_slots(n));
+  size_t off = kWsLookback;
+  p.u_word = reinterpret_cast<uint64_t*>(w + off);
+  p.ck = 1;
   p.need_fixup = (op == TC_OP_REDUCE && (mode == MODE_TILES || mode == MODE_GENERAL) &&
                   (kTileElems % seg != 0))
                      ? 1

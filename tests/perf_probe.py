@@ -58,5 +58,39 @@ def main():
                       f"{gbs:7.0f} GB/s {100 * gbs / PEAK:5.1f}%", flush=True)
 
 
+def full_probe():
+    import os
+
+    dev = torch.device("cuda:0")
+    for log2n in ((30,) if os.environ.get("TC_DEBUG") else (30, 33)):
+        n = 1 << log2n
+        x = torch.empty(n, dtype=torch.float16, device=dev)
+        for lo in range(0, n, 1 << 28):
+            x[lo:lo + (1 << 28)] = torch.rand(min(1 << 28, n - lo), device=dev)
+        y = torch.empty(n, dtype=torch.float32, device=dev)
+        y16 = torch.empty(n, dtype=torch.float16, device=dev)
+        for k, lag in (("1", "1"), ("1", "3"), ("1", "5"), ("1", "6"), ("1", "7"), ("2", "1"),
+                       ("2", "2"), ("2", "3"), ("3", "1"), ("4", "1")):
+            os.environ["TC_CHUNK_TILES"] = k
+            os.environ["TC_CHUNK_LAG"] = lag
+            for dt, o, out in ((torch.float32, 4, y), (torch.float16, 2, y16)):
+                ms = timeit(lambda: D.full_scan(x, dt, exclusive=True, out=out), reps=5, warm=2)
+                gbs = (2 + o) * n / ms / 1e6
+                print(f"full excl scan 2^{log2n} K={k:>2} L={lag} {str(dt):14} {ms:8.3f} ms "
+                      f"{n / ms / 1e6:7.1f} Gelem/s {gbs:7.0f} GB/s {100 * gbs / PEAK:5.1f}%",
+                      flush=True)
+        os.environ.pop("TC_CHUNK_TILES")
+        for s_ in (1 << 19, 1 << 22):
+            ms = timeit(lambda: D.seg_scan(x, s_, torch.float32, out=y), reps=5, warm=2)
+            gbs = 6 * n / ms / 1e6
+            print(f"seg scan 2^{log2n} s={s_} f32 {ms:8.3f} ms {gbs:7.0f} GB/s {100 * gbs / PEAK:5.1f}%",
+                  flush=True)
+        del x, y, y16
+        torch.cuda.empty_cache()
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["full"]:
+        full_probe()
+        sys.exit(0)
     main()

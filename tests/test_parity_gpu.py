@@ -163,6 +163,36 @@ def test_scan_carry_in_total_out(n, cuda, rng):
     assert tot.item() == last
 
 
+@pytest.mark.parametrize("k", ["1", "2", "3", "4"])
+def test_chunked_scan_modes(k, cuda, monkeypatch):
+    """MODE_CHUNK (full scans, segments > 2^18, carry-in): P1/P2 chunk
+    walk at several unit sizes (TC_CHUNK_TILES), ragged lengths, long
+    non-power-of-two segments, inclusive/exclusive, with and without a
+    carry -- bit-exact on sparse-ones data (every prefix an exact integer)."""
+    monkeypatch.setenv("TC_CHUNK_TILES", k)
+    rs = np.random.default_rng(int(k))
+    for n in ((1 << 22) + 1234, 3 << 20, 8192 * 300 + 5):
+        x = (rs.random(n) < 1 / 16).astype(np.float16)
+        xd = torch.from_numpy(x).to(cuda)
+        for s in (n, 300001, (1 << 18) + 8192, 1 << 20):
+            for exc in (False, True):
+                exp = O.ref_seg_scan(x, s, inclusive=not exc)
+                got = D.seg_scan(xd, s, torch.float32, exclusive=exc).cpu().numpy()
+                assert np.array_equal(got, exp.astype(np.float32)), (n, s, exc)
+        cin = torch.tensor([5.0], dtype=torch.float64, device=cuda)
+        tot = torch.zeros(1, dtype=torch.float64, device=cuda)
+        for s in (n, 4096):
+            got = D.seg_scan(xd, s, torch.float32, exclusive=True, carry_in=cin, total_out=tot)
+            exp = O.ref_seg_scan(x, s, inclusive=False, carry=5.0)
+            assert np.array_equal(got.cpu().numpy(), exp.astype(np.float32)), (n, s)
+            assert tot.item() == O.ref_seg_scan(x, s, carry=5.0)[-1]
+        # deterministic across reruns (fixed composition order)
+        g = torch.rand(n, device=cuda).to(torch.float16)
+        a = D.full_scan(g, torch.float32)
+        b = D.full_scan(g, torch.float32)
+        assert torch.equal(a, b)
+
+
 # ------------------------------------------------ non-integer data tolerance
 
 
