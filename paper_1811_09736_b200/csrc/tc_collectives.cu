@@ -179,8 +179,15 @@ struct Cfg {
   static constexpr int STAGES =
       CHUNK ? 8 : (OP == OP_REDUCE) ? (MINB == 2 ? 6 : 8) : (MINB == 2 ? 4 : 6);
   static constexpr int ACC = CHUNK ? 8 : 4;  // TMEM accumulator stages (tiles)
-  // warps: TMA, MMA, 4 epilogue (+ CHUNK: the prefix warp)
-  static constexpr int THREADS = CHUNK ? kThreads + 32 : kThreads;
+  // CHUNK with one granule per row splits the epilogue: warps 2..5 write the
+  // prefix sums, warps 6..9 ("aggregate warps") fold row totals into unit
+  // aggregates and publish them
+  static constexpr bool AGG = CHUNK && GR == 1;
+  // warps: TMA, MMA, 4 epilogue (+ AGG: 4 aggregate) (+ CHUNK: the prefix warp)
+  static constexpr int THREADS = kThreads + (AGG ? 128 : 0) + (CHUNK ? 32 : 0);
+  // arrivals that free a TMEM slot: per thread (128), or lane 0 of the 4
+  // output + 4 aggregate warps
+  static constexpr int TEMPTY = AGG ? 8 : kEpiThreads;
   static constexpr int TMEM_COLS = pow2_at_least(ACC * N);
   static constexpr int OUT_BUFS = (OP == OP_SCAN) ? ((sizeof(OutT) == 4 && MINB == 2) ? 1 : 2) : 0;
   static constexpr uint32_t OUT_BYTES = kTileElems * sizeof(OutT);
@@ -209,6 +216,9 @@ struct Misc {
   double fa[2][4];
   float ov[2][4];
   int of[2][4];
+  float apv[2][4];  // aggregate warps' exchange
+  int apf[2][4];
+  double apd[2][4];
   uint64_t pfull[4];   // CHUNK: prefix warp -> epilogue (entry value of unit j ready)
   uint64_t pempty[4];  // CHUNK: epilogue -> prefix warp (slot consumed)
   double entry[4];
@@ -543,7 +553,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
     }
     for (int a = 0; a < ACC; ++a) {
       ptx::mbar_init(&misc->tfull[a], 1);
-      ptx::mbar_init(&misc->tempty[a], kEpiThreads);
+      ptx::mbar_init(&misc->tempty[a], C::TEMPTY);
     }
     for (int k = 0; k < 4; ++k) {
       ptx::mbar_init(&misc->pfull[k], 1);
@@ -655,253 +665,172 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
     };
 
     if constexpr (OP == OP_SCAN && MODE == MODE_CHUNK && GR == 1) {
-      // ---- CHUNK with one granule (= one row) per segment step: fused
-      // steps.  Step s runs the A pass of tile s and the O pass of tile
-      // s - L*K of this CTA's sequence, sharing one TMEM wait and one
-      // cross-warp exchange barrier.  Tiles with a segment start use
-      // (value, flag) pair scans; all others plain row-total scans.
-      const long long lk = p.lag * ck;
+      // ---- CHUNK, one granule per row: OUTPUT warps.  Tile s of this
+      // CTA's sequence: wait for its X.U in TMEM, take the unit's entry value
+      // from the prefix warp at the unit's first tile, then exactly the plain
+      // row-scan epilogue (pair scans only in tiles holding a segment start).
+      // The aggregate warps (6..9) read the same TMEM slots independently.
       const long long ntc =
           n_units ? (n_units - 1) * ck + (unit_t1(n_units - 1) - unit_t0(n_units - 1)) : 0;
       auto row_start = [&](long long row) -> int {
         return (static_cast<uint32_t>(row) % static_cast<uint32_t>(p.m) == 0) && row <= p.qlast &&
                !(row == 0 && has_carry);
       };
-      long long ja = 0, ka = 0, jo = 0, ko = 0;  // (unit, tile-in-unit) of the A / O tiles
       const bool excl = p.exclusive != 0;
-      double pacc = 0.0;  // this row's totals of start-free tiles not yet folded into u_v
-      double u_v = 0.0;   // unit aggregate so far (all threads hold the same value)
-      int u_f = 0;
-      int bpar = 0;       // exchange-buffer parity, flips once per exchange barrier
-      for (long long s2 = 0; s2 < ntc + lk; ++s2) {
-        const bool has_a = s2 < ntc;
-        const long long so = s2 - lk;
-        const bool has_o = so >= 0;
-        long long ta = 0, to = 0;
-        bool last_a = false, first_o = false, st_a = false, st_o = false;
-        const long long ja_c = ja, jo_c = jo;
-        if (has_a) {
-          ta = unit_t0(ja) + ka;
-          last_a = (ka == ck - 1) || (ta == T - 1);
-          st_a = tile_has_start(ta);
-          if (++ka == ck) {
-            ka = 0;
-            ++ja;
-          }
+      long long jo = 0, ko = 0;
+      static_assert(ACC == 8, "CHUNK epilogue assumes 8 TMEM tile slots");
+      for (long long s2 = 0; s2 < ntc; ++s2) {
+        const long long to = unit_t0(jo) + ko;
+        const bool first_o = (ko == 0);
+        const bool st_o = tile_has_start(to);
+        const long long jo_c = jo;
+        if (++ko == ck) {
+          ko = 0;
+          ++jo;
         }
-        if (has_o) {
-          to = unit_t0(jo) + ko;
-          first_o = (ko == 0);
-          st_o = tile_has_start(to);
-          if (++ko == ck) {
-            ko = 0;
-            ++jo;
-          }
-        }
-        // ---- TMEM: row total of tile A, full X.U row of tile O
-        const int sa = static_cast<int>(s2 & (ACC - 1));
-        const int sl_o = has_o ? static_cast<int>(so & (ACC - 1)) : 0;
-        uint32_t ra[1];
+        const int par = static_cast<int>(s2 & 1);
+        const int sl = static_cast<int>(s2 & 7);
         uint32_t ro[64];
-        if (has_a) ptx::mbar_wait_warp(&misc->tfull[sa], static_cast<uint32_t>((s2 >> 3) & 1));
-        static_assert(ACC == 8, "fused CHUNK epilogue assumes 8 TMEM tile slots");
+        ptx::mbar_wait_warp(&misc->tfull[sl], static_cast<uint32_t>((s2 >> 3) & 1));
         ptx::tc_fence_after();
-        if (has_a) ptx::tmem_ld_32x32b<1>(tmem + lane_base + sa * N + 63, ra);
-        if (has_o) {
+        {
           uint32_t(&r0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&ro[0]);
           uint32_t(&r1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&ro[32]);
-          ptx::tmem_ld_32x32b<32>(tmem + lane_base + sl_o * N, r0);
-          ptx::tmem_ld_32x32b<32>(tmem + lane_base + sl_o * N + 32, r1);
+          ptx::tmem_ld_32x32b<32>(tmem + lane_base + sl * N, r0);
+          ptx::tmem_ld_32x32b<32>(tmem + lane_base + sl * N + 32, r1);
         }
         ptx::tmem_wait_ld();
-        if (has_o) {
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(&misc->tempty[sl_o]);
-        }
-        // ---- A part, warp level
-        const long long row_a = ta * kTileRows + rit;
-        float tot_a = __uint_as_float(ra[0]);
-        if (has_a && row_a == p.rows_full) {  // ragged last row: outside the TMA view
-          float acc = 0.f;
-#pragma unroll  // (a rolled loop here would keep ptxas from proving reconvergence)
-          for (int k = 0; k < kRow; ++k) {
-            const long long e = row_a * kRow + k;
-            if (e < p.n) acc += __half2float(p.x[e]);
-          }
-          tot_a = acc;
-        }
-        const bool bar_a = has_a && (st_a || last_a);
-        if (has_a && !st_a) pacc += static_cast<double>(tot_a);
-        __syncwarp();  // reconverge (ragged-row loop) so the shuffles below stay plain SHFL
-        if (bar_a) {
-          if (st_a) {
-            float v = tot_a;
-            int f = row_start(row_a);
-            warp_pair_scan(v, f, lane);
-            if (lane == 31) {
-              misc->pv[bpar][qd] = v;  // A tile pairs per warp
-              misc->pf[bpar][qd] = f;
-            }
-          }
-          const double pw = warp_sum_d(pacc);
-          if (lane == 0) misc->pd[bpar][qd] = pw;
-        }
-        // ---- O part, warp level
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&misc->tempty[sl]);
         float vv[64];
+#pragma unroll
+        for (int k = 0; k < 64; ++k) vv[k] = __uint_as_float(ro[k]);
         const long long row_o = to * kTileRows + rit;
+        if (row_o == p.rows_full) {  // ragged last row: recompute the row scan from HBM
+          float acc = 0.f;
+#pragma unroll
+          for (int k = 0; k < 64; ++k) {
+            const long long e = row_o * kRow + k;
+            acc += (e < p.n) ? __half2float(p.x[e]) : 0.f;
+            vv[k] = acc;
+          }
+        }
+        if (first_o) {  // value entering the unit, from the prefix warp
+          const int ps = static_cast<int>(jo_c & 3);
+          ptx::mbar_wait_warp(&misc->pfull[ps], static_cast<uint32_t>((jo_c >> 2) & 1));
+          carry = misc->entry[ps];
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&misc->pempty[ps]);
+        }
+        if (leader) ptx::bulk_wait_read<C::OUT_BUFS - 1>();  // staging buffer free
+        __syncwarp();
+        const float tot = vv[63];
         float o_ex = 0.f, o_ve = 0.f;
         int o_fe = 0;
-        if (has_o) {
-#pragma unroll
-          for (int k = 0; k < 64; ++k) vv[k] = __uint_as_float(ro[k]);
-          if (row_o == p.rows_full) {  // ragged last row: recompute the row scan from HBM
-            float acc = 0.f;
-#pragma unroll
-            for (int k = 0; k < 64; ++k) {
-              const long long e = row_o * kRow + k;
-              acc += (e < p.n) ? __half2float(p.x[e]) : 0.f;
-              vv[k] = acc;
-            }
+        if (!st_o) {
+          const float incl = warp_incl_scan(tot, lane);
+          o_ex = __shfl_up_sync(kFull, incl, 1);
+          if (lane == 0) o_ex = 0.f;
+          if (lane == 31) misc->ov[par][qd] = incl;
+        } else {
+          float v = tot;
+          int f = row_start(row_o);
+          warp_pair_scan(v, f, lane);
+          o_ve = __shfl_up_sync(kFull, v, 1);
+          o_fe = __shfl_up_sync(kFull, f, 1);
+          if (lane == 0) {
+            o_ve = 0.f;
+            o_fe = 0;
           }
-          if (leader) ptx::bulk_wait_read<C::OUT_BUFS - 1>();  // staging buffer free
-          __syncwarp();
-          const float tot = vv[63];
-          if (!st_o) {
-            const float incl = warp_incl_scan(tot, lane);
-            o_ex = __shfl_up_sync(kFull, incl, 1);
-            if (lane == 0) o_ex = 0.f;
-            if (lane == 31) misc->ov[bpar][qd] = incl;
-          } else {
-            float v = tot;
-            int f = row_start(row_o);
-            warp_pair_scan(v, f, lane);
-            o_ve = __shfl_up_sync(kFull, v, 1);
-            o_fe = __shfl_up_sync(kFull, f, 1);
-            if (lane == 0) {
-              o_ve = 0.f;
-              o_fe = 0;
-            }
-            if (lane == 31) {
-              misc->ov[bpar][qd] = v;
-              misc->of[bpar][qd] = f;
-            }
+          if (lane == 31) {
+            misc->ov[par][qd] = v;
+            misc->of[par][qd] = f;
           }
         }
-        if (!bar_a && !has_o) continue;  // uniform: no exchange this step
         ptx::named_bar_sync(kEpiBar, kEpiThreads);
-        // ---- A part, block level: fold into the unit; publish at its end
-        if (bar_a) {
-          u_v += ((misc->pd[bpar][0] + misc->pd[bpar][1]) + misc->pd[bpar][2]) +
-                 misc->pd[bpar][3];
-          pacc = 0.0;
-          if (st_a) {
-            float tv = 0.f;
-            int tf = 0;
+        float off;
+        if (!st_o) {
+          float woff = 0.f, ttot = 0.f;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) compose(tv, tf, misc->pv[bpar][k], misc->pf[bpar][k]);
-            u_v = tf ? static_cast<double>(tv) : u_v + static_cast<double>(tv);
-            u_f |= tf;
+          for (int k = 0; k < 4; ++k) {
+            const float y = misc->ov[par][k];
+            if (k < qd) woff += y;
+            ttot += y;
           }
-          if (last_a) {
-            if (leader) chunk_publish(p.u_word + ja_c * Gc + cta, u_v, u_f, ep);
-            u_v = 0.0;
-            u_f = 0;
+          off = static_cast<float>(carry + static_cast<double>(o_ex + woff));
+          carry += static_cast<double>(ttot);
+        } else {
+          float wv = 0.f, tv = 0.f;
+          int wf = 0, tf = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float yv = misc->ov[par][k];
+            const int yf = misc->of[par][k];
+            if (k < qd) compose(wv, wf, yv, yf);
+            compose(tv, tf, yv, yf);
           }
+          compose(wv, wf, o_ve, o_fe);
+          off = row_start(row_o) ? 0.f
+                                 : (wf ? wv : static_cast<float>(carry + static_cast<double>(wv)));
+          carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
         }
-        if (has_o) {
-          // ---- O part, block level.  The entry value is awaited only now,
-          // after this step's A aggregate went out (keeps the L-unit slack).
-          if (first_o) {
-            const int ps = static_cast<int>(jo_c & 3);
-            ptx::mbar_wait_warp(&misc->pfull[ps], static_cast<uint32_t>((jo_c >> 2) & 1));
-            carry = misc->entry[ps];
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&misc->pempty[ps]);
-          }
-          float off;
-          if (!st_o) {
-            float woff = 0.f, ttot = 0.f;
+        auto outv = [&](int e) -> float {
+          if (excl) return (e == 0) ? (off + 0.f) : (vv[e - 1] + off);
+          return vv[e] + off;
+        };
+        if (p.total_out && row_o == (p.n - 1) / kRow) {
+          const int k = static_cast<int>((p.n - 1) % kRow);
+          float incl = 0.f;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float y = misc->ov[bpar][k];
-              if (k < qd) woff += y;
-              ttot += y;
-            }
-            off = static_cast<float>(carry + static_cast<double>(o_ex + woff));
-            carry += static_cast<double>(ttot);
-          } else {
-            float wv = 0.f, tv = 0.f;
-            int wf = 0, tf = 0;
+          for (int e = 0; e < 64; ++e)
+            if (e == k) incl = vv[e] + off;
+          *p.total_out = static_cast<double>(incl);
+        }
+        uint8_t* stg = smem + C::OFF_OUT + (C::OUT_BUFS == 2 ? par : 0) * C::OUT_BYTES;
+        const uint32_t rb = static_cast<uint32_t>(rit) * 128u;
+        const uint32_t sw = static_cast<uint32_t>(rit & 7);
+        if constexpr (sizeof(OutT) == 2) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float yv = misc->ov[bpar][k];
-              const int yf = misc->of[bpar][k];
-              if (k < qd) compose(wv, wf, yv, yf);
-              compose(tv, tf, yv, yf);
-            }
-            compose(wv, wf, o_ve, o_fe);
-            off = row_start(row_o) ? 0.f
-                                   : (wf ? wv : static_cast<float>(carry + static_cast<double>(wv)));
-            carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
+          for (int c = 0; c < 8; ++c) {
+            uint4 w;
+            __half2 h0 = __floats2half2_rn(outv(8 * c + 0), outv(8 * c + 1));
+            __half2 h1 = __floats2half2_rn(outv(8 * c + 2), outv(8 * c + 3));
+            __half2 h2 = __floats2half2_rn(outv(8 * c + 4), outv(8 * c + 5));
+            __half2 h3 = __floats2half2_rn(outv(8 * c + 6), outv(8 * c + 7));
+            w.x = *reinterpret_cast<uint32_t*>(&h0);
+            w.y = *reinterpret_cast<uint32_t*>(&h1);
+            w.z = *reinterpret_cast<uint32_t*>(&h2);
+            w.w = *reinterpret_cast<uint32_t*>(&h3);
+            *reinterpret_cast<uint4*>(stg + rb + ((c ^ sw) << 4)) = w;
           }
-          auto outv = [&](int e) -> float {
-            if (excl) return (e == 0) ? (off + 0.f) : (vv[e - 1] + off);
-            return vv[e] + off;
-          };
-          if (p.total_out && row_o == (p.n - 1) / kRow) {
-            const int k = static_cast<int>((p.n - 1) % kRow);
-            float incl = 0.f;
+        } else {
 #pragma unroll
-            for (int e = 0; e < 64; ++e)
-              if (e == k) incl = vv[e] + off;
-            *p.total_out = static_cast<double>(incl);
-          }
-          uint8_t* stg = smem + C::OFF_OUT + (C::OUT_BUFS == 2 ? (so & 1) : 0) * C::OUT_BYTES;
-          const uint32_t rb = static_cast<uint32_t>(rit) * 128u;
-          const uint32_t sw = static_cast<uint32_t>(rit & 7);
-          if constexpr (sizeof(OutT) == 2) {
+          for (int h = 0; h < 2; ++h) {
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-              uint4 w;
-              __half2 h0 = __floats2half2_rn(outv(8 * c + 0), outv(8 * c + 1));
-              __half2 h1 = __floats2half2_rn(outv(8 * c + 2), outv(8 * c + 3));
-              __half2 h2 = __floats2half2_rn(outv(8 * c + 4), outv(8 * c + 5));
-              __half2 h3 = __floats2half2_rn(outv(8 * c + 6), outv(8 * c + 7));
-              w.x = *reinterpret_cast<uint32_t*>(&h0);
-              w.y = *reinterpret_cast<uint32_t*>(&h1);
-              w.z = *reinterpret_cast<uint32_t*>(&h2);
-              w.w = *reinterpret_cast<uint32_t*>(&h3);
-              *reinterpret_cast<uint4*>(stg + rb + ((c ^ sw) << 4)) = w;
+              float4 w = make_float4(outv(32 * h + 4 * c + 0), outv(32 * h + 4 * c + 1),
+                                     outv(32 * h + 4 * c + 2), outv(32 * h + 4 * c + 3));
+              *reinterpret_cast<float4*>(stg + h * 16384 + rb + ((c ^ sw) << 4)) = w;
             }
-          } else {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-#pragma unroll
-              for (int c = 0; c < 8; ++c) {
-                float4 w = make_float4(outv(32 * h + 4 * c + 0), outv(32 * h + 4 * c + 1),
-                                       outv(32 * h + 4 * c + 2), outv(32 * h + 4 * c + 3));
-                *reinterpret_cast<float4*>(stg + h * 16384 + rb + ((c ^ sw) << 4)) = w;
-              }
-            }
-          }
-          if (row_o == p.rows_full) {  // ragged last row: direct stores
-            OutT* out = reinterpret_cast<OutT*>(p.out);
-#pragma unroll
-            for (int k = 0; k < 64; ++k) {
-              const long long e = row_o * kRow + k;
-              if (e < p.n) out[e] = cvt_out<OutT>(outv(k));
-            }
-          }
-          ptx::fence_proxy_async_smem();
-          ptx::named_bar_sync(kEpiBar, kEpiThreads);
-          if (leader) {
-            const int32_t r0 = static_cast<int32_t>(to * kTileRows);
-            ptx::tma_store_2d(&tout, stg, 0, r0);
-            if constexpr (sizeof(OutT) == 4) ptx::tma_store_2d(&tout, stg + 16384, 32, r0);
-            ptx::bulk_commit();
           }
         }
-        bpar ^= 1;
+        if (row_o == p.rows_full) {  // ragged last row: direct stores
+          OutT* out = reinterpret_cast<OutT*>(p.out);
+#pragma unroll
+          for (int k = 0; k < 64; ++k) {
+            const long long e = row_o * kRow + k;
+            if (e < p.n) out[e] = cvt_out<OutT>(outv(k));
+          }
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(kEpiBar, kEpiThreads);
+        if (leader) {
+          const int32_t r0 = static_cast<int32_t>(to * kTileRows);
+          ptx::tma_store_2d(&tout, stg, 0, r0);
+          if constexpr (sizeof(OutT) == 4) ptx::tma_store_2d(&tout, stg + 16384, 32, r0);
+          ptx::bulk_commit();
+        }
       }
     } else {
       walk_epi([&](int i, int it, long long t, int pass, long long uj, bool first, bool last) {
@@ -1358,6 +1287,99 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
           p.hdr->ticket = 0u;
           __threadfence();
         }
+      }
+    }
+  } else if (C::AGG && warp < 10) {
+    // ================= aggregate warps (CHUNK, one granule per row) =========
+    // Tile s: read only the row totals (TMEM column 63), fold start-free
+    // tiles into a per-thread fp64 sum, compose (value, has-start) pairs in
+    // tiles holding a segment start; at the unit's last tile publish the
+    // unit aggregate as one fence-free 64-bit word.  Runs ahead of the output
+    // warps by up to the 8 TMEM slots, which is the slack that hides the
+    // publish -> observe latency from the other CTAs' prefix warps.
+    if constexpr (C::AGG) {
+      const int qa = warp & 3;
+      const int ra = qa * 32 + lane;
+      const int ea = threadIdx.x - 192;
+      const bool has_carry = (p.carry_in != nullptr);
+      const uint32_t ep = (p.hdr->epoch + 1u) & 0x3FFFFFFFu;
+      const uint32_t lb = static_cast<uint32_t>(qa * 32) << 16;
+      constexpr uint32_t kAggBar = 2;
+      const long long ntc =
+          n_units ? (n_units - 1) * ck + (unit_t1(n_units - 1) - unit_t0(n_units - 1)) : 0;
+      double pacc = 0.0, u_v = 0.0;
+      int u_f = 0, bpar = 0;
+      long long ja = 0, ka = 0;
+      for (long long s2 = 0; s2 < ntc; ++s2) {
+        const long long ta = unit_t0(ja) + ka;
+        const bool last_a = (ka == ck - 1) || (ta == T - 1);
+        const long long ja_c = ja;
+        if (++ka == ck) {
+          ka = 0;
+          ++ja;
+        }
+        const long long r0 = ta * kTileRows;
+        bool st_a;
+        {
+          const uint32_t m32 = static_cast<uint32_t>(p.m);
+          long long fs = static_cast<long long>(static_cast<uint32_t>(r0) / m32) * m32;
+          if (fs < r0) fs += m32;
+          if (fs == 0 && has_carry) fs = m32;
+          st_a = fs < r0 + kTileRows && fs <= p.qlast;
+        }
+        const int sl = static_cast<int>(s2 & 7);
+        uint32_t r1[1];
+        ptx::mbar_wait_warp(&misc->tfull[sl], static_cast<uint32_t>((s2 >> 3) & 1));
+        ptx::tc_fence_after();
+        ptx::tmem_ld_32x32b<1>(tmem + lb + sl * N + 63, r1);
+        ptx::tmem_wait_ld();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&misc->tempty[sl]);
+        const long long row = r0 + ra;
+        float tot = __uint_as_float(r1[0]);
+        if (row == p.rows_full) {  // ragged last row: outside the TMA view
+          float acc = 0.f;
+#pragma unroll
+          for (int k = 0; k < kRow; ++k) {
+            const long long e = row * kRow + k;
+            if (e < p.n) acc += __half2float(p.x[e]);
+          }
+          tot = acc;
+        }
+        __syncwarp();
+        if (!st_a) pacc += static_cast<double>(tot);
+        if (!(st_a || last_a)) continue;  // uniform
+        if (st_a) {
+          float v = tot;
+          int f = (static_cast<uint32_t>(row) % static_cast<uint32_t>(p.m) == 0) &&
+                  row <= p.qlast && !(row == 0 && has_carry);
+          warp_pair_scan(v, f, lane);
+          if (lane == 31) {
+            misc->apv[bpar][qa] = v;
+            misc->apf[bpar][qa] = f;
+          }
+        }
+        const double pw = warp_sum_d(pacc);
+        if (lane == 0) misc->apd[bpar][qa] = pw;
+        ptx::named_bar_sync(kAggBar, kEpiThreads);
+        u_v += ((misc->apd[bpar][0] + misc->apd[bpar][1]) + misc->apd[bpar][2]) +
+               misc->apd[bpar][3];
+        pacc = 0.0;
+        if (st_a) {
+          float tv = 0.f;
+          int tf = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) compose(tv, tf, misc->apv[bpar][k], misc->apf[bpar][k]);
+          u_v = tf ? static_cast<double>(tv) : u_v + static_cast<double>(tv);
+          u_f |= tf;
+        }
+        if (last_a) {
+          if (ea == 0) chunk_publish(p.u_word + ja_c * Gc + cta, u_v, u_f, ep);
+          u_v = 0.0;
+          u_f = 0;
+        }
+        bpar ^= 1;
       }
     }
   } else {
