@@ -17,10 +17,11 @@ for p in $PARTS; do
       timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?"; tail -c 3000 "$OUT/bench.json"; tail -5 "$OUT/bench.err"
       timeout 600 python bench.py --impl reference > "$OUT/bench_ref.json" 2> "$OUT/bench_ref.err"; echo "bench ref rc=$?"; cut -c1-400 "$OUT/bench_ref.json";;
     launches)
-      timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 120 --csv \
-        --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 3 --no-extras --no-cpu --e2e-steps 1 > "$OUT/launches_bench.log" 2>&1; echo "launches rc=$?";;
+      timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
+        --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 1 > "$OUT/launches_bench.log" 2>&1; echo "launches rc=$?";;
     prof)
-      for cfg in "reduce 16 f16" "reduce 256 f16" "reduce 65536 f16" "scan 256 f16" "scan 16384 f32"; do
+      CFGS=("reduce 16 f16" "reduce 2048 f16" "reduce 65536 f16" "scan 256 f16" "scan 16384 f32" "scan 1073741824 f32" "scan 300 f16")
+      for cfg in "${CFGS[@]}"; do
         set -- $cfg
         timeout 600 ncu --set full --clock-control none --import-source on -k regex:seg_kernel -s 2 -c 1 \
           -o "$OUT/prof_$1_$2_$3" -f python tests/prof_one.py $1 $2 $3 30 3 > "$OUT/prof_$1_$2_$3.log" 2>&1; echo "prof $cfg rc=$?"

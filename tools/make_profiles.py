@@ -57,24 +57,30 @@ def main():
     ours = [x for x in ls if "tc::seg_kernel" in x[1]]
     by = defaultdict(list)
     for lid, name, grid, m in ours:
-        key = name.split("(")[0].replace("void ", "")
+        # group by instantiation and input size (bench sweep 2^30 vs e2e chunks 2^27)
+        gb = round(m.get("dram__bytes_read.sum", 0) / 2 ** 30, 1)
+        key = (name.split("(")[0].replace("void ", ""), gb)
         by[key].append((grid, m))
     lines = ["# Launch list (ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
              "dram__bytes_write.sum --clock-control none)", "",
              f"Source: `{lf.relative_to(ROOT)}` of session `{tag}` (bench.py --steps 2 "
-             "--no-extras). Cold-cache, serialised: compare shares, not absolutes.", "",
+             "--warmup 3 --no-cpu --e2e-steps 1, first 400 launches). Cold-cache, "
+             "serialised: compare shares, not absolutes.", "",
              f"Total launches: {len(ls)}; tc::seg_kernel launches: {len(ours)}", "",
-             "| kernel | grid | launches | mean us | DRAM read GB | DRAM write MB |",
-             "|---|---|---|---|---|---|"]
+             "| kernel | input | grid | launches | mean us | DRAM read GB | DRAM write MB |",
+             "|---|---|---|---|---|---|---|"]
     tot = sum(m.get("gpu__time_duration.sum", 0) for _, _, _, m in ours)
     rd_all = []
     for key, v in by.items():
         t = statistics.mean(m["gpu__time_duration.sum"] for _, m in v) / 1e3
         rd = statistics.mean(m.get("dram__bytes_read.sum", 0) for _, m in v)
         wr = statistics.mean(m.get("dram__bytes_write.sum", 0) for _, m in v)
-        rd_all.extend(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
-                      for _, m in v)
-        lines.append(f"| `{key}` | {v[0][0]} | {len(v)} | {t:.1f} | {rd / 1e9:.4f} | "
+        kname, gb = key
+        if kname.startswith("tc::seg_kernel<0,") and gb >= 1.5:  # the 2^30 sweep launches
+            rd_all.extend(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
+                          for _, m in v)
+        size = "2^30" if gb >= 1.5 else "2^27 (e2e chunk)"
+        lines.append(f"| `{kname}` | {size} | {v[0][0]} | {len(v)} | {t:.1f} | {rd / 1e9:.4f} | "
                      f"{wr / 1e6:.2f} |")
     lines += ["", f"tc::seg_kernel total device time in the list: {tot / 1e6:.3f} ms"]
     (dst / "launches_summary.md").write_text("\n".join(lines) + "\n")
@@ -82,7 +88,7 @@ def main():
         (ROOT / "profiles" / "traffic.json").write_text(json.dumps({
             "per_launch_bytes": statistics.mean(rd_all),
             "what": "mean dram__bytes_read.sum + dram__bytes_write.sum per tc::seg_kernel "
-                    "reduce launch of the bench sweep (2^30 fp16 input)",
+                    "reduce launch of the bench sweep (2^30 fp16 input, 13 segment sizes)",
             "source": f"profiles/{rnd}/launches_summary.md",
         }, indent=1) + "\n")
 
