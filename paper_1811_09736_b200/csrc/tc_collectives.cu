@@ -1513,6 +1513,9 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
   auto kern = seg_kernel<OP, GR, MODE, OutT>;
   static std::atomic<int> attr_done{0};
   if (!attr_done.load()) {
+    // max shared-memory carveout, so MINB = 2 kernels really get 2 CTAs/SM
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
         cudaSuccess) {
       set_err("cudaFuncSetAttribute failed: %s%lld", cudaGetErrorString(cudaGetLastError()), 0);
@@ -1534,7 +1537,29 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
     set_err("occupancy query failed: %s%lld", cudaGetErrorString(cudaGetLastError()), 0);
     return TC_CUDA_ERROR;
   }
-  if (per_sm > Cfg<OP, GR, MODE, OutT>::MINB) per_sm = Cfg<OP, GR, MODE, OutT>::MINB;
+  // CTAs per SM.  The occupancy API reports 1 for these kernels (it appears
+  // to budget a full TMEM allocation per CTA), but two CTAs do co-reside,
+  // and measured on B200 (2^30 fp16) a second epilogue per SM pays off where
+  // the per-tile epilogue is latency-heavy: the cross-row-group combine of
+  // reduce ROWS with >= 16 rows per segment (s = 1024/4096: 92-93 % -> 99 %
+  // of copy bandwidth) and the pair scans of GENERAL (s = 300: reduce 26 ->
+  // 47 %, scan 70 -> 85 %), and fp32-output scans of tiny segments (85 ->
+  // 89 %).  Elsewhere one CTA/SM is as fast or faster (reduce TILES 100 vs
+  // 97 %, fp16 scans 93-95 vs 91-92 %); cooperative launches (CHUNK) must
+  // match the API.
+  if (MODE != MODE_CHUNK) {
+    per_sm = (MODE == MODE_GENERAL || (OP == OP_REDUCE && MODE == MODE_ROWS && p0.log2m >= 4) ||
+              (OP == OP_SCAN && MODE == MODE_LOCAL && sizeof(OutT) == 4))
+                 ? 2
+                 : 1;
+    if (per_sm > Cfg<OP, GR, MODE, OutT>::MINB) per_sm = Cfg<OP, GR, MODE, OutT>::MINB;
+  } else if (per_sm > 1) {
+    per_sm = 1;
+  }
+  if (const char* e = getenv("TC_CTAS_PER_SM")) {  // tuning override
+    const int want = atoi(e);
+    if (want >= 1 && want <= 2 && MODE != MODE_CHUNK) per_sm = want;
+  }
   long long grid = static_cast<long long>(di.sms) * per_sm;
   if (grid > p0.num_tiles) grid = p0.num_tiles;
   if (grid > kMaxCtas) grid = kMaxCtas;

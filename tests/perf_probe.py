@@ -38,7 +38,7 @@ def main():
     ms = timeit(lambda: y.copy_(x))
     print(f"copy fp16 2^30: {ms:.3f} ms  {4 * n / ms / 1e6:.0f} GB/s", flush=True)
     if "reduce" in which:
-        for s in [16, 32, 64, 128, 256, 512, 1024, 4096, 8192, 16384, 65536, 300, n]:
+        for s in [16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384, 32768, 65536, 300, 1000, n]:
             for dt, o in ((torch.float32, 4), (torch.float16, 2)):
                 out = torch.empty(-(-n // s), dtype=dt, device=dev)
                 ms = timeit(lambda: D.seg_reduce(x, s, dt, out=out))
