@@ -65,6 +65,7 @@ extern "C" {
 #define TC_F16 0
 #define TC_F32 1
 #define TC_F64 2               /* reduce only: fp64 partial for NCCL combine */
+#define TC_BF16 3              /* input only (the *_ex entry points): bfloat16 */
 
 /* op ids for tc_workspace_bytes */
 #define TC_OP_REDUCE 0
@@ -79,6 +80,13 @@ size_t tc_workspace_bytes(int op, int64_t n, int64_t seg);
  * Replaces segmented_reduce (reduce.py:379). */
 int tc_seg_reduce(const void* x, int64_t n, int64_t seg, void* out,
                   int out_dtype, void* ws, size_t ws_bytes, void* stream);
+
+/* Same with an explicit input dtype: TC_F16 (binary16, as above) or TC_BF16
+ * (bfloat16: same tcgen05 kind::f16 MMA with BF16 A/B operands, fp32
+ * accumulation).  Extension beyond the reference (fp16 only), SURVEY.md
+ * section 8(f)3. */
+int tc_seg_reduce_ex(const void* x, int in_dtype, int64_t n, int64_t seg, void* out,
+                     int out_dtype, void* ws, size_t ws_bytes, void* stream);
 
 /* Full sum of n elements into out[0] (one output).  Replaces grid_reduce
  * (reduce.py:332).  Equivalent to tc_seg_reduce with seg = n. */
@@ -99,6 +107,11 @@ int tc_seg_scan(const void* x, int64_t n, int64_t seg, void* out,
                 int out_dtype, int exclusive, const double* carry_in,
                 double* total_out, void* ws, size_t ws_bytes, void* stream);
 
+/* Same with an explicit input dtype (TC_F16 | TC_BF16), see tc_seg_reduce_ex. */
+int tc_seg_scan_ex(const void* x, int in_dtype, int64_t n, int64_t seg, void* out, int out_dtype,
+                   int exclusive, const double* carry_in, double* total_out, void* ws,
+                   size_t ws_bytes, void* stream);
+
 /* Full (one-segment) scan.  Replaces grid_scan (scan.py:249). */
 int tc_full_scan(const void* x, int64_t n, void* out, int out_dtype,
                  int exclusive, const double* carry_in, double* total_out,
@@ -115,7 +128,7 @@ const char* tc_last_error(void);
 uint64_t tc_launch_count(void);
 void tc_reset_launch_count(void);
 
-/* ABI version: (major << 16) | minor. */
+/* ABI version: (major << 16) | minor.  1.1 added the *_ex entry points. */
 int tc_abi_version(void);
 
 #ifdef __cplusplus

@@ -52,12 +52,17 @@ def workspace(op: int, n: int, seg: int, device: torch.device) -> torch.Tensor:
     return ws
 
 
+_IN = {torch.float16: _lib.TC_F16, torch.bfloat16: _lib.TC_BF16}
+
+
 def _prep(x: torch.Tensor) -> torch.Tensor:
+    """fp16 (the reference's input type) or bf16 (extension) stay as they
+    are; anything else is converted to fp16 like reduce._as_flat_half."""
     if not x.is_cuda:
         raise ValueError("device entry points take CUDA tensors")
     if x.dim() != 1:
         raise BadLengthError("collectives operate on flat vectors")
-    if x.dtype != torch.float16:
+    if x.dtype not in _IN:
         x = x.to(torch.float16)
     if not x.is_contiguous() or x.data_ptr() % 16:
         x = x.contiguous().clone()
@@ -76,8 +81,9 @@ def seg_reduce(x: torch.Tensor, seg: int, out_dtype=torch.float16, out=None) -> 
     if out is None:
         out = torch.empty(nseg, dtype=out_dtype, device=x.device)
     ws = workspace(_lib.TC_OP_REDUCE, n, seg, x.device)
-    _check(_lib.lib.tc_seg_reduce(x.data_ptr(), n, seg, out.data_ptr(), _DT[out.dtype],
-                                  ws.data_ptr(), ws.numel(), _stream_ptr(x.device)))
+    _check(_lib.lib.tc_seg_reduce_ex(x.data_ptr(), _IN[x.dtype], n, seg, out.data_ptr(),
+                                     _DT[out.dtype], ws.data_ptr(), ws.numel(),
+                                     _stream_ptr(x.device)))
     return out
 
 
@@ -90,8 +96,9 @@ def full_reduce(x: torch.Tensor, out_dtype=torch.float16, out=None) -> torch.Ten
     if out is None:
         out = torch.empty(1, dtype=out_dtype, device=x.device)
     ws = workspace(_lib.TC_OP_REDUCE, n, n, x.device)
-    _check(_lib.lib.tc_full_reduce(x.data_ptr(), n, out.data_ptr(), _DT[out.dtype],
-                                   ws.data_ptr(), ws.numel(), _stream_ptr(x.device)))
+    _check(_lib.lib.tc_seg_reduce_ex(x.data_ptr(), _IN[x.dtype], n, n, out.data_ptr(),
+                                     _DT[out.dtype], ws.data_ptr(), ws.numel(),
+                                     _stream_ptr(x.device)))
     return out
 
 
@@ -113,9 +120,9 @@ def seg_scan(x: torch.Tensor, seg: int, out_dtype=torch.float16, exclusive=False
     ws = workspace(_lib.TC_OP_SCAN, n, seg, x.device)
     cin = carry_in.data_ptr() if carry_in is not None else None
     tout = total_out.data_ptr() if total_out is not None else None
-    _check(_lib.lib.tc_seg_scan(x.data_ptr(), n, seg, out.data_ptr(), _DT[out.dtype],
-                                1 if exclusive else 0, cin, tout, ws.data_ptr(), ws.numel(),
-                                _stream_ptr(x.device)))
+    _check(_lib.lib.tc_seg_scan_ex(x.data_ptr(), _IN[x.dtype], n, seg, out.data_ptr(),
+                                   _DT[out.dtype], 1 if exclusive else 0, cin, tout,
+                                   ws.data_ptr(), ws.numel(), _stream_ptr(x.device)))
     return out
 
 

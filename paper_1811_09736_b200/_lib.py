@@ -26,6 +26,7 @@ TC_NO_DEVICE = 6
 TC_F16 = 0
 TC_F32 = 1
 TC_F64 = 2
+TC_BF16 = 3
 
 TC_OP_REDUCE = 0
 TC_OP_SCAN = 1
@@ -39,6 +40,11 @@ SIGNATURES = {
     "tc_workspace_bytes": (_size, [ctypes.c_int, _i64, _i64]),
     "tc_seg_reduce": (ctypes.c_int, [_c_void_p, _i64, _i64, _c_void_p, ctypes.c_int,
                                      _c_void_p, _size, _c_void_p]),
+    "tc_seg_reduce_ex": (ctypes.c_int, [_c_void_p, ctypes.c_int, _i64, _i64, _c_void_p,
+                                        ctypes.c_int, _c_void_p, _size, _c_void_p]),
+    "tc_seg_scan_ex": (ctypes.c_int, [_c_void_p, ctypes.c_int, _i64, _i64, _c_void_p, ctypes.c_int,
+                                      ctypes.c_int, _c_void_p, _c_void_p, _c_void_p, _size,
+                                      _c_void_p]),
     "tc_full_reduce": (ctypes.c_int, [_c_void_p, _i64, _c_void_p, ctypes.c_int,
                                       _c_void_p, _size, _c_void_p]),
     "tc_seg_scan": (ctypes.c_int, [_c_void_p, _i64, _i64, _c_void_p, ctypes.c_int, ctypes.c_int,

@@ -63,6 +63,7 @@
 //    MMA numerics            engine.py:326-348 (products exact, one rounding)
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -111,7 +112,8 @@ constexpr size_t kWsEntries = 1024;
 constexpr size_t kWsLookback = kWsEntries + sizeof(Entry) * 2 * kMaxCtas;
 
 struct Params {
-  const __half* x;
+  const __half* x;      // input bits (binary16, or bfloat16 when in_bf16)
+  int in_bf16;          // input dtype: 0 = fp16, 1 = bf16 (same MMA kind::f16, other A/B format)
   void* out;
   long long n;          // elements
   long long seg;        // segment size
@@ -235,12 +237,12 @@ constexpr uint32_t smem_bytes() {
 // Constant B operand, K-major, 128-B swizzled: row n (N index) holds B[k][n]
 // for k = 0..63.  Reduce: granule indicator.  Scan: block-diag upper-tri U.
 template <int OP, int GR, int N>
-__device__ void build_b(uint8_t* sb) {
+__device__ void build_b(uint8_t* sb, uint16_t one_bits) {
   constexpr int G = 64 / GR;
   for (int idx = threadIdx.x; idx < N * 8; idx += blockDim.x) {
     const int n = idx >> 3, pos = idx & 7;
     const int lc = pos ^ (n & 7);  // logical 16-B chunk stored at physical position pos
-    __align__(16) __half h[8];
+    __align__(16) uint16_t h[8];  // 1.0 in the input's format (fp16 0x3C00, bf16 0x3F80)
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const int k = lc * 8 + e;
@@ -249,7 +251,7 @@ __device__ void build_b(uint8_t* sb) {
         one = (n < GR) && (k / G == n);
       else
         one = (k / G == n / G) && (k <= n);
-      h[e] = __float2half_rn(one ? 1.f : 0.f);
+      h[e] = one ? one_bits : 0;
     }
     *reinterpret_cast<uint4*>(sb + n * 128 + pos * 16) = *reinterpret_cast<uint4*>(h);
   }
@@ -295,27 +297,43 @@ __device__ __forceinline__ float warp_incl_scan(float v, int lane) {
   return v;
 }
 
+// One input element as float (binary16 or bfloat16 bits).
+__device__ __forceinline__ float in_to_float(const __half* x, long long e, bool bf16) {
+  const unsigned short b = __ldg(reinterpret_cast<const unsigned short*>(x) + e);
+  return bf16 ? __uint_as_float(static_cast<uint32_t>(b) << 16)
+              : __half2float(__ushort_as_half(b));
+}
+
 // Sum of x[lo, hi) in fp64 by the 128 epilogue threads (all get the result).
 template <typename MiscT>
-__device__ double epi_range_sum(const __half* x, long long lo, long long hi, int et, int lane,
-                                int qd, MiscT* misc) {
+__device__ double epi_range_sum(const __half* x, bool bf16, long long lo, long long hi, int et,
+                                int lane, int qd, MiscT* misc) {
   double acc = 0.0;
   if (hi > lo) {
     long long a = (lo + 7) & ~7LL;  // 16-B aligned start
     if (a > hi) a = hi;
     if (et == 0)
-      for (long long e = lo; e < a; ++e) acc += __half2float(x[e]);
+      for (long long e = lo; e < a; ++e) acc += in_to_float(x, e, bf16);
     const long long nb = (hi - a) >> 3;  // whole 8-element blocks
     const uint4* xv = reinterpret_cast<const uint4*>(x + a);
     float fs = 0.f;
     int cnt = 0;
     for (long long b = et; b < nb; b += kEpiThreads) {
       const uint4 w = __ldg(xv + b);
-      const __half2* h = reinterpret_cast<const __half2*>(&w);
+      if (bf16) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 f2 = __half22float2(h[k]);
-        fs += f2.x + f2.y;
+        for (int k = 0; k < 4; ++k) {
+          const float2 f2 = __bfloat1622float2(h[k]);
+          fs += f2.x + f2.y;
+        }
+      } else {
+        const __half2* h = reinterpret_cast<const __half2*>(&w);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f2 = __half22float2(h[k]);
+          fs += f2.x + f2.y;
+        }
       }
       if (++cnt == 64) {  // flush to fp64 every 512 elements
         acc += fs;
@@ -325,7 +343,7 @@ __device__ double epi_range_sum(const __half* x, long long lo, long long hi, int
     }
     acc += fs;
     if (et == kEpiThreads - 1)
-      for (long long e = a + nb * 8; e < hi; ++e) acc += __half2float(x[e]);
+      for (long long e = a + nb * 8; e < hi; ++e) acc += in_to_float(x, e, bf16);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
@@ -567,7 +585,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
     ptx::tmem_alloc(&misc->tmem_base, C::TMEM_COLS);
     ptx::tmem_relinquish();
   }
-  build_b<OP, GR, N>(smem + C::OFF_B);
+  build_b<OP, GR, N>(smem + C::OFF_B, p.in_bf16 ? 0x3F80 : 0x3C00);
   ptx::fence_proxy_async_smem();  // B written by the generic proxy, read by the tensor core
   ptx::tc_fence_before();
   __syncthreads();
@@ -590,7 +608,9 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
   } else if (warp == 1) {
     // ================= MMA issuer (one thread) =================
     if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_f16_f32(128, N);
+      // kind::f16 with fp32 D; A/B format F16 or BF16 (idesc bits 7-9 / 10-12)
+      const uint32_t idesc =
+          ptx::idesc_f16_f32(128, N) | (p.in_bf16 ? ((1u << 7) | (1u << 10)) : 0u);
       const uint64_t bdesc = ptx::smem_desc_sw128(smem + C::OFF_B);
       walk_tiles([&](int i, long long) {
         const int s = i % STAGES;
@@ -638,7 +658,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
       // segment that precede the range, re-read from HBM (bounded by
       // kScanPrepassMax), plus the caller's carry for segment 0.
       const long long seg_start = (range_first_elem / p.seg) * p.seg;
-      carry = epi_range_sum(p.x, seg_start, range_first_elem, et, lane, qd, misc);
+      carry = epi_range_sum(p.x, p.in_bf16 != 0, seg_start, range_first_elem, et, lane, qd, misc);
       if (seg_start == 0 && has_carry) carry += *p.carry_in;
     }
 
@@ -712,7 +732,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
 #pragma unroll
           for (int k = 0; k < 64; ++k) {
             const long long e = row_o * kRow + k;
-            acc += (e < p.n) ? __half2float(p.x[e]) : 0.f;
+            acc += (e < p.n) ? in_to_float(p.x, e, p.in_bf16 != 0) : 0.f;
             vv[k] = acc;
           }
         }
@@ -876,7 +896,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
               float s = 0.f;
               for (int k = 0; k < G; ++k) {
                 const long long e = e0 + j * G + k;
-                if (e < p.n) s += __half2float(p.x[e]);
+                if (e < p.n) s += in_to_float(p.x, e, p.in_bf16 != 0);
               }
               gs[j] = s;
             }
@@ -1009,7 +1029,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
             for (int k = 0; k < 64; ++k) {
               if (k % G == 0) s = 0.f;
               const long long e = e0 + k;
-              s += (e < p.n) ? __half2float(p.x[e]) : 0.f;
+              s += (e < p.n) ? in_to_float(p.x, e, p.in_bf16 != 0) : 0.f;
               vv[k] = s;
             }
           }
@@ -1343,7 +1363,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
 #pragma unroll
           for (int k = 0; k < kRow; ++k) {
             const long long e = row * kRow + k;
-            if (e < p.n) acc += __half2float(p.x[e]);
+            if (e < p.n) acc += in_to_float(p.x, e, p.in_bf16 != 0);
           }
           tot = acc;
         }
@@ -1575,7 +1595,8 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
   const char* wsb = reinterpret_cast<const char*>(p.hdr);
   const void* in_base = p.rows_full > 0 ? static_cast<const void*>(p.x)
                                         : static_cast<const void*>(wsb + kWsZeroRow);
-  if (!make_map(&tin, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, in_base,
+  if (!make_map(&tin, p.in_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                2, in_base,
                 p.rows_full > 0 ? p.rows_full : 1, kRow)) {
     set_err("cuTensorMapEncodeTiled (input) failed%s%lld", "", 0);
     return TC_CUDA_ERROR;
@@ -1747,13 +1768,18 @@ size_t tc_workspace_bytes(int op, int64_t n, int64_t seg) {
   return ws_need(op, n, seg);
 }
 
-int tc_seg_reduce(const void* x, int64_t n, int64_t seg, void* out, int out_dtype, void* ws,
-                  size_t ws_bytes, void* stream) {
+int tc_seg_reduce_ex(const void* x, int in_dtype, int64_t n, int64_t seg, void* out, int out_dtype,
+                     void* ws, size_t ws_bytes, void* stream) {
   g_err[0] = 0;
   int rc = common_checks(x, n, seg, out, out_dtype, false, ws, ws_bytes, TC_OP_REDUCE);
   if (rc) return rc;
+  if (in_dtype != TC_F16 && in_dtype != TC_BF16) {
+    set_err("unsupported input dtype %s%lld", "", in_dtype);
+    return TC_BAD_CONFIG;
+  }
   int gr = 0, mode = 0;
   Params p = make_params(x, n, seg, out, ws, TC_OP_REDUCE, false, &gr, &mode);
+  p.in_bf16 = (in_dtype == TC_BF16) ? 1 : 0;
   LaunchFn fn = nullptr;
   int es = 2;
   if (out_dtype == TC_F16) {
@@ -1773,20 +1799,30 @@ int tc_seg_reduce(const void* x, int64_t n, int64_t seg, void* out, int out_dtyp
   return fn(p, es, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int tc_seg_reduce(const void* x, int64_t n, int64_t seg, void* out, int out_dtype, void* ws,
+                  size_t ws_bytes, void* stream) {
+  return tc_seg_reduce_ex(x, TC_F16, n, seg, out, out_dtype, ws, ws_bytes, stream);
+}
+
 int tc_full_reduce(const void* x, int64_t n, void* out, int out_dtype, void* ws, size_t ws_bytes,
                    void* stream) {
   return tc_seg_reduce(x, n, n < 1 ? 1 : n, out, out_dtype, ws, ws_bytes, stream);
 }
 
-int tc_seg_scan(const void* x, int64_t n, int64_t seg, void* out, int out_dtype, int exclusive,
-                const double* carry_in, double* total_out, void* ws, size_t ws_bytes,
-                void* stream) {
+int tc_seg_scan_ex(const void* x, int in_dtype, int64_t n, int64_t seg, void* out, int out_dtype,
+                   int exclusive, const double* carry_in, double* total_out, void* ws,
+                   size_t ws_bytes, void* stream) {
   g_err[0] = 0;
   int rc = common_checks(x, n, seg, out, out_dtype, true, ws, ws_bytes, TC_OP_SCAN);
   if (rc) return rc;
+  if (in_dtype != TC_F16 && in_dtype != TC_BF16) {
+    set_err("unsupported input dtype %s%lld", "", in_dtype);
+    return TC_BAD_CONFIG;
+  }
   int gr = 0, mode = 0;
   Params p = make_params(x, n, seg, out, ws, TC_OP_SCAN, carry_in != nullptr, &gr, &mode);
   p.exclusive = exclusive ? 1 : 0;
+  p.in_bf16 = (in_dtype == TC_BF16) ? 1 : 0;
   p.carry_in = carry_in;
   p.total_out = total_out;
   LaunchFn fn =
@@ -1796,6 +1832,13 @@ int tc_seg_scan(const void* x, int64_t n, int64_t seg, void* out, int out_dtype,
     return TC_BAD_CONFIG;
   }
   return fn(p, out_dtype == TC_F16 ? 2 : 4, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int tc_seg_scan(const void* x, int64_t n, int64_t seg, void* out, int out_dtype, int exclusive,
+                const double* carry_in, double* total_out, void* ws, size_t ws_bytes,
+                void* stream) {
+  return tc_seg_scan_ex(x, TC_F16, n, seg, out, out_dtype, exclusive, carry_in, total_out, ws,
+                        ws_bytes, stream);
 }
 
 int tc_full_scan(const void* x, int64_t n, void* out, int out_dtype, int exclusive,
@@ -1823,6 +1866,6 @@ const char* tc_last_error(void) { return g_err; }
 uint64_t tc_launch_count(void) { return g_launches; }
 void tc_reset_launch_count(void) { g_launches = 0; }
 
-int tc_abi_version(void) { return (1 << 16) | 0; }
+int tc_abi_version(void) { return (1 << 16) | 1; }
 
 }  // extern "C"

@@ -66,6 +66,11 @@ def test_c_abi_argument_errors_before_launch():
     # scans have no fp64 output
     assert L.tc_seg_scan(x, 100, 16, out, _lib.TC_F64, 0, None, None, wsp, 60000, None) == _lib.TC_BAD_CONFIG
     assert "segment size" in _lib.last_error() or "dtype" in _lib.last_error()
+    # *_ex: unknown input dtype -> bad config, before any launch
+    assert L.tc_seg_reduce_ex(x, 7, 100, 16, out, _lib.TC_F32, wsp, 60000, None) == _lib.TC_BAD_CONFIG
+    assert "input dtype" in _lib.last_error()
+    assert L.tc_seg_scan_ex(x, 7, 100, 16, out, _lib.TC_F32, 0, None, None, wsp, 60000,
+                            None) == _lib.TC_BAD_CONFIG
 
 
 def test_select_algorithm_matches_reference_table(golden):

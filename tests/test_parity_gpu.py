@@ -193,6 +193,31 @@ def test_chunked_scan_modes(k, cuda, monkeypatch):
         assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("n", [1000, (1 << 20) + 77, (1 << 22) + 1234])
+def test_bf16_input(n, cuda, rng):
+    """bf16 input (tcgen05 kind::f16 with BF16 operands; extension beyond the
+    fp16-only reference): bit-exact on small integers (exact in bf16 and in
+    every partial sum), and within the fp32 tolerance on uniform data, across
+    the LOCAL / ROWS / TILES / GENERAL / CHUNK modes."""
+    xi = rng.integers(0, 8, n).astype(np.float32)
+    xd = torch.from_numpy(xi).to(cuda).to(torch.bfloat16)
+    x64 = xd.double().cpu().numpy()
+    for s in (16, 48, 256, 8192, 300, 1 << 19, n):
+        got = D.seg_reduce(xd, s, torch.float32).cpu().numpy()
+        assert np.array_equal(got, O.ref_seg_reduce(x64, s).astype(np.float32)), (n, s)
+        for exc in (False, True):
+            got = D.seg_scan(xd, s, torch.float32, exclusive=exc).cpu().numpy()
+            exp = O.ref_seg_scan(x64, s, inclusive=not exc).astype(np.float32)
+            assert np.array_equal(got, exp), (n, s, exc)
+    xu = torch.rand(n, device=cuda).to(torch.bfloat16)
+    u64 = xu.double().cpu().numpy()
+    for s in (64, 1000, n):
+        assert_close(D.seg_reduce(xu, s, torch.float32).cpu().numpy(), O.ref_seg_reduce(u64, s),
+                     np.float32)
+        assert_close(D.seg_scan(xu, s, torch.float32).cpu().numpy(), O.ref_seg_scan(u64, s),
+                     np.float32)
+
+
 # ------------------------------------------------ non-integer data tolerance
 
 
