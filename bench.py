@@ -452,6 +452,34 @@ def run_extras(args, x, dev, world, rank, barrier, max_over_ranks, peak):
     out["scan_sweep_f16"] = {"workload": "segmented inclusive scan fp16, 2^30 per GPU, fp16 out",
                              "rows": rows}
     del y
+    # widened rows: bf16 input, non-power-of-two segment sizes
+    xb = x.to(torch.bfloat16)
+    rows = []
+    for s in (16, 256, 4096, 65536):
+        o = torch.empty(-(-n // s), dtype=torch.float16, device=dev)
+        ms = _time_op(lambda: D.seg_reduce(xb, s, torch.float16, out=o), reps, 2, stream,
+                      barrier, max_over_ranks)
+        b = reduce_bytes(n, s)
+        rows.append({"seg": s, "ms": round(ms, 4), "gbs_per_gpu": round(b / ms / 1e6, 1),
+                     "frac": round(b / ms / 1e6 / peak, 4)})
+    out["reduce_bf16_input"] = {"workload": "segmented reduce, 2^30 bf16 per GPU, fp16 out",
+                                "rows": rows}
+    del xb
+    rows = []
+    y = torch.empty(n, dtype=torch.float16, device=dev)
+    for s in (48, 300, 1000, 100000):
+        o = torch.empty(-(-n // s), dtype=torch.float16, device=dev)
+        ms = _time_op(lambda: D.seg_reduce(x, s, torch.float16, out=o), reps, 2, stream,
+                      barrier, max_over_ranks)
+        b = reduce_bytes(n, s)
+        ms2 = _time_op(lambda: D.seg_scan(x, s, torch.float16, out=y), reps, 2, stream,
+                       barrier, max_over_ranks)
+        rows.append({"seg": s, "reduce_ms": round(ms, 4),
+                     "reduce_frac": round(b / ms / 1e6 / peak, 4), "scan_ms": round(ms2, 4),
+                     "scan_frac": round(4 * n / ms2 / 1e6 / peak, 4)})
+    out["non_pow2_segments"] = {"workload": "segmented reduce / inclusive scan, 2^30 fp16, "
+                                            "fp16 out, ragged last segment", "rows": rows}
+    del y
     # full ops over 2^33 elements sharded across the ranks
     nf = 1 << FULL_LOG2N
     lo, hi = PD.even_bounds(nf, world, rank)

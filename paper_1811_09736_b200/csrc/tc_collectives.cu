@@ -953,16 +953,22 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
             }
           } else {
             // MODE_GENERAL: segmented (value, has_end) pair scan over rows
-            long long rem = p.m - 1 - qmod;  // granules until the next segment end
-            long long sg = qdiv;             // segment containing granule q0 + j
-            const long long seg0 = sg;       // segment closed by the row's first end
+            // segment ends inside the row, in 32-bit granule offsets: the first
+            // at p.m - 1 - qmod, then every p.m; the input's last granule ends
+            // the ragged last segment
+            const long long rem0 = p.m - 1 - qmod;
+            const long long dl = p.qlast - q0;
+            const int lastj = dl < GR ? static_cast<int>(dl) : GR;
+            const int m32 = p.m < (1LL << 20) ? static_cast<int>(p.m) : (1 << 20);
+            int e = rem0 < GR ? static_cast<int>(rem0) : GR;
+            long long sg = qdiv;        // segment containing granule q0 + j
+            const long long seg0 = sg;  // segment closed by the row's first end
             float run = 0.f, head = 0.f;
             int seen = 0;
   #pragma unroll
             for (int j = 0; j < GR; ++j) {
               run += gs[j];
-              const long long qj = q0 + j;
-              if (qj <= p.qlast && (rem == 0 || qj == p.qlast)) {
+              if ((j == e && j <= lastj) || j == lastj) {
                 if (!seen) {
                   head = run;  // needs the carry from earlier rows / tiles
                   seen = 1;
@@ -971,8 +977,8 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
                 }
                 ++sg;
                 run = 0.f;
+                e += m32;
               }
-              rem = (rem == 0) ? p.m - 1 : rem - 1;
             }
             float v = run;
             int f = seen;
@@ -1109,20 +1115,28 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
             float run = 0.f;
             int seen = 0;
             {
+              // segment starts inside the row (32-bit granule offsets): the first
+              // at (m - q0 % m) % m, then every m; none past the input's end,
+              // and granule 0 continues the caller's segment when carried in
               const long long qm = (MODE == MODE_GENERAL) ? qmod : (q0 % p.m);
-              long long rem = qm == 0 ? 0 : p.m - qm;  // granules until the next start
+              const long long r0 = qm == 0 ? 0 : p.m - qm;
+              const long long dl = p.qlast - q0;
+              const int lastj = dl < GR ? static_cast<int>(dl) : GR;
+              const int m32 = p.m < (1LL << 20) ? static_cast<int>(p.m) : (1 << 20);
+              int nx = r0 < GR ? static_cast<int>(r0) : GR;
+              const bool skip0 = (q0 == 0 && has_carry);
   #pragma unroll
               for (int j = 0; j < GR; ++j) {
-                const bool st =
-                    (rem == 0) && (q0 + j <= p.qlast) && !((q0 + j) == 0 && has_carry);
-                if (st) {
-                  run = 0.f;
-                  seen = 1;
+                if (j == nx) {
+                  if (j <= lastj && !(j == 0 && skip0)) {
+                    run = 0.f;
+                    seen = 1;
+                  }
+                  nx += m32;
                 }
                 off[j] = run;
                 chain[j] = !seen;
                 run += vv[j * G + G - 1];
-                rem = (rem == 0) ? p.m - 1 : rem - 1;
               }
             }
             float v = run;
