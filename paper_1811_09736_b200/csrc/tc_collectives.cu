@@ -177,9 +177,16 @@ struct Cfg {
   static constexpr int N = (OP == OP_SCAN) ? 64 : (GR < 16 ? 16 : GR);  // UMMA N
   static constexpr bool CHUNK = (MODE == MODE_CHUNK);
   // CTAs per SM (CHUNK keeps 2-4 units of tiles in TMEM: all 512 columns, 1 CTA/SM)
-  static constexpr int MINB = (CHUNK || (OP == OP_SCAN && GR >= 32)) ? 1 : 2;
-  static constexpr int STAGES =
-      CHUNK ? 8 : (OP == OP_REDUCE) ? (MINB == 2 ? 6 : 8) : (MINB == 2 ? 4 : 6);
+  // GENERAL reduce with 8..32 granules per row runs 3 CTAs/SM: its per-tile
+  // granule walk is latency-bound, so a third resident epilogue pays
+  // (measured on B200, 2^30 fp16: s = 300 58 -> 78 %, s = 1000 86 -> 93 %
+  // of copy bandwidth; GR = 4 (s = 48) is faster at 2, 95 vs 89 %)
+  static constexpr int MINB = (CHUNK || (OP == OP_SCAN && GR >= 32)) ? 1
+                              : (OP == OP_REDUCE && MODE == MODE_GENERAL && GR >= 8 && GR <= 32) ? 3
+                                                                                       : 2;
+  static constexpr int STAGES = CHUNK ? 8
+                                : (OP == OP_REDUCE) ? (MINB == 3 ? 4 : MINB == 2 ? 6 : 8)
+                                                    : (MINB == 2 ? 4 : 6);
   static constexpr int ACC = CHUNK ? 8 : 4;  // TMEM accumulator stages (tiles)
   // CHUNK with one granule per row splits the epilogue: warps 2..5 write the
   // prefix sums, warps 6..9 ("aggregate warps") fold row totals into unit
@@ -1577,13 +1584,15 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
   // the per-tile epilogue is latency-heavy: the cross-row-group combine of
   // reduce ROWS with >= 16 rows per segment (s = 1024/4096: 92-93 % -> 99 %
   // of copy bandwidth) and the pair scans of GENERAL (s = 300: reduce 26 ->
-  // 47 %, scan 70 -> 85 %), and fp32-output scans of tiny segments (85 ->
+  // 47 %, scan 70 -> 85 %; GENERAL reduce with 8..32 granules per row takes
+  // 3, see Cfg::MINB), and fp32-output scans of tiny segments (85 ->
   // 89 %).  Elsewhere one CTA/SM is as fast or faster (reduce TILES 100 vs
   // 97 %, fp16 scans 93-95 vs 91-92 %); cooperative launches (CHUNK) must
   // match the API.
   if (MODE != MODE_CHUNK) {
-    per_sm = (MODE == MODE_GENERAL || (OP == OP_REDUCE && MODE == MODE_ROWS && p0.log2m >= 4) ||
-              (OP == OP_SCAN && MODE == MODE_LOCAL && sizeof(OutT) == 4))
+    per_sm = (MODE == MODE_GENERAL) ? Cfg<OP, GR, MODE, OutT>::MINB
+             : ((OP == OP_REDUCE && MODE == MODE_ROWS && p0.log2m >= 4) ||
+                (OP == OP_SCAN && MODE == MODE_LOCAL && sizeof(OutT) == 4))
                  ? 2
                  : 1;
     if (per_sm > Cfg<OP, GR, MODE, OutT>::MINB) per_sm = Cfg<OP, GR, MODE, OutT>::MINB;
@@ -1592,7 +1601,7 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
   }
   if (const char* e = getenv("TC_CTAS_PER_SM")) {  // tuning override
     const int want = atoi(e);
-    if (want >= 1 && want <= 2 && MODE != MODE_CHUNK) per_sm = want;
+    if (want >= 1 && want <= Cfg<OP, GR, MODE, OutT>::MINB && MODE != MODE_CHUNK) per_sm = want;
   }
   long long grid = static_cast<long long>(di.sms) * per_sm;
   if (grid > p0.num_tiles) grid = p0.num_tiles;
