@@ -117,6 +117,29 @@ int tc_full_scan(const void* x, int64_t n, void* out, int out_dtype,
                  int exclusive, const double* carry_in, double* total_out,
                  void* ws, size_t ws_bytes, void* stream);
 
+/* Irregular segments (extension; the paper elides
+ * them, "irregular segmented reduction is implemented in terms
+ * of regular segmented reduction").  Segment k covers
+ * x[offsets[k], offsets[k+1]) for k < nseg; `offsets` is a DEVICE array of
+ * nseg + 1 non-decreasing int64 with offsets[0] = 0 and offsets[nseg] = n
+ * (empty segments allowed; the Python shim validates it, the kernels only
+ * stay memory-safe on malformed offsets).  in_dtype TC_F16 | TC_BF16.
+ * Same tile product as the regular path (the in-row prefix X.U on the tensor
+ * core), with each row's segment starts taken from `offsets`.
+ *
+ * tc_irreg_reduce: out[k] = sum of segment k (0 for an empty one), out_dtype
+ *   TC_F16 | TC_F32 | TC_F64.  One launch. */
+int tc_irreg_reduce(const void* x, int in_dtype, int64_t n, const int64_t* offsets, int64_t nseg,
+                    void* out, int out_dtype, void* ws, size_t ws_bytes, void* stream);
+
+/* tc_irreg_scan: inclusive (exclusive != 0: exclusive) prefix sums restarted
+ * at every segment start, n outputs (TC_F16 | TC_F32).  Two launches: the
+ * carry each CTA range hands on (reads only the range tails behind the last
+ * segment start), then the tile scan. */
+int tc_irreg_scan(const void* x, int in_dtype, int64_t n, const int64_t* offsets, int64_t nseg,
+                  void* out, int out_dtype, int exclusive, void* ws, size_t ws_bytes,
+                  void* stream);
+
 /* Human-readable name of a status code. */
 const char* tc_status_string(int status);
 
@@ -128,7 +151,8 @@ const char* tc_last_error(void);
 uint64_t tc_launch_count(void);
 void tc_reset_launch_count(void);
 
-/* ABI version: (major << 16) | minor.  1.1 added the *_ex entry points. */
+/* ABI version: (major << 16) | minor.  1.1 added the *_ex entry points,
+ * 1.2 the tc_irreg_* entry points. */
 int tc_abi_version(void);
 
 #ifdef __cplusplus

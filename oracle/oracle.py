@@ -170,6 +170,57 @@ def ref_seg_scan_exact(values, seg_size, inclusive=True, carry=None):
     return c.reshape(-1)[:n]
 
 
+# ----------------------------------------- irregular (CSR-offset) segments
+# Extension: the reference has no irregular entry
+# point (the paper elides it), so these restate the exact
+# oracle (oracle.py:47-75: binary64 per-segment sums / prefix sums) for
+# segments values[offsets[k]:offsets[k+1]].
+
+
+def random_offsets(rng, n, mean_len, empty_frac=0.0):
+    """nseg + 1 non-decreasing offsets over [0, n]: segment lengths
+    geometric with the given mean, a fraction of them forced empty."""
+    lens = rng.geometric(1.0 / max(1.0, float(mean_len)), size=max(4, 2 * n // max(1, int(mean_len)) + 8))
+    if empty_frac > 0:
+        lens[rng.random(lens.size) < empty_frac] = 0
+    ends = np.cumsum(lens)
+    ends = ends[ends < n]
+    off = np.concatenate([[0], ends, [n]]).astype(np.int64)
+    return off
+
+
+def ref_irreg_reduce(values, offsets):
+    """Exact binary64 sums of values[offsets[k]:offsets[k+1]] (0 if empty)."""
+    x = np.asarray(values).astype(np.float64)
+    off = np.asarray(offsets, dtype=np.int64)
+    out = np.zeros(off.size - 1, dtype=np.float64)
+    ne = off[1:] > off[:-1]
+    if ne.any():
+        out[ne] = np.add.reduceat(x, off[:-1][ne])
+    return out
+
+
+def ref_irreg_scan(values, offsets, inclusive=True):
+    """Per-segment prefix sums (exclusive: 0 at each segment start), from an
+    extended-precision running sum (np.longdouble: the subtraction of the
+    segment base costs < 2^-60 relative, far below any tolerance used)."""
+    x = np.asarray(values).astype(np.longdouble)
+    off = np.asarray(offsets, dtype=np.int64)
+    n = x.size
+    c = np.cumsum(x)
+    seg = np.searchsorted(off, np.arange(n), side="right") - 1
+    st = off[seg]
+    base = np.where(st > 0, c[np.maximum(st - 1, 0)], 0)
+    incl = c - base
+    if inclusive:
+        return incl.astype(np.float64)
+    ex = np.empty_like(incl)
+    ex[1:] = incl[:-1]
+    ex[0] = 0
+    ex[np.arange(n) == st] = 0
+    return ex.astype(np.float64)
+
+
 # ------------------------------------------------ tile-engine arithmetic (sim)
 
 

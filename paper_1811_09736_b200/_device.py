@@ -132,3 +132,58 @@ def full_scan(x: torch.Tensor, out_dtype=torch.float16, exclusive=False,
     """One-segment scan of the whole vector (tc_full_scan)."""
     x = _prep(x)
     return seg_scan(x, max(x.numel(), 1), out_dtype, exclusive, carry_in, total_out, out)
+
+
+def _prep_offsets(offsets: torch.Tensor, n: int, device: torch.device, validate: bool) -> torch.Tensor:
+    """int64 CUDA offsets (nseg + 1 entries, offsets[0] = 0, offsets[-1] = n,
+    non-decreasing).  ``validate`` checks that on the device (one host sync)."""
+    if not isinstance(offsets, torch.Tensor):
+        raise ValueError("device entry points take CUDA tensors")
+    if offsets.dim() != 1 or offsets.numel() < 2:
+        raise BadLengthError("offsets must be a flat vector of nseg + 1 >= 2 entries")
+    offsets = offsets.to(device=device, dtype=torch.int64)
+    if not offsets.is_contiguous():
+        offsets = offsets.contiguous()
+    if validate:
+        ok = ((offsets[0] == 0) & (offsets[-1] == n)
+              & (offsets[1:] >= offsets[:-1]).all())
+        if not bool(ok):
+            raise BadConfigError(
+                "offsets must be non-decreasing with offsets[0] = 0 and offsets[-1] = len(values)")
+    return offsets
+
+
+def irreg_reduce(x: torch.Tensor, offsets: torch.Tensor, out_dtype=torch.float16, out=None,
+                 validate: bool = True) -> torch.Tensor:
+    """Sums of the irregular segments x[offsets[k]:offsets[k+1]] (tc_irreg_reduce)."""
+    x = _prep(x)
+    n = x.numel()
+    if n == 0:
+        raise BadLengthError("input must be a non-empty flat vector")
+    offsets = _prep_offsets(offsets, n, x.device, validate)
+    nseg = offsets.numel() - 1
+    if out is None:
+        out = torch.empty(nseg, dtype=out_dtype, device=x.device)
+    ws = workspace(_lib.TC_OP_REDUCE, n, n, x.device)
+    _check(_lib.lib.tc_irreg_reduce(x.data_ptr(), _IN[x.dtype], n, offsets.data_ptr(), nseg,
+                                    out.data_ptr(), _DT[out.dtype], ws.data_ptr(), ws.numel(),
+                                    _stream_ptr(x.device)))
+    return out
+
+
+def irreg_scan(x: torch.Tensor, offsets: torch.Tensor, out_dtype=torch.float16, exclusive=False,
+               out=None, validate: bool = True) -> torch.Tensor:
+    """Prefix sums restarted at every offsets[k] (tc_irreg_scan)."""
+    x = _prep(x)
+    n = x.numel()
+    if n == 0:
+        raise BadLengthError("input must be a non-empty flat vector")
+    offsets = _prep_offsets(offsets, n, x.device, validate)
+    nseg = offsets.numel() - 1
+    if out is None:
+        out = torch.empty(n, dtype=out_dtype, device=x.device)
+    ws = workspace(_lib.TC_OP_SCAN, n, n, x.device)
+    _check(_lib.lib.tc_irreg_scan(x.data_ptr(), _IN[x.dtype], n, offsets.data_ptr(), nseg,
+                                  out.data_ptr(), _DT[out.dtype], 1 if exclusive else 0,
+                                  ws.data_ptr(), ws.numel(), _stream_ptr(x.device)))
+    return out

@@ -51,6 +51,10 @@ SIGNATURES = {
                                    _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
     "tc_full_scan": (ctypes.c_int, [_c_void_p, _i64, _c_void_p, ctypes.c_int, ctypes.c_int,
                                     _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
+    "tc_irreg_reduce": (ctypes.c_int, [_c_void_p, ctypes.c_int, _i64, _c_void_p, _i64, _c_void_p,
+                                       ctypes.c_int, _c_void_p, _size, _c_void_p]),
+    "tc_irreg_scan": (ctypes.c_int, [_c_void_p, ctypes.c_int, _i64, _c_void_p, _i64, _c_void_p,
+                                     ctypes.c_int, ctypes.c_int, _c_void_p, _size, _c_void_p]),
     "tc_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "tc_last_error": (ctypes.c_char_p, []),
     "tc_launch_count": (ctypes.c_uint64, []),

@@ -242,6 +242,17 @@ __host__ __device__ constexpr uint32_t idesc_f16_f32(int m, int n) {
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+// named barrier that also returns how many participating threads passed pred
+__device__ __forceinline__ uint32_t named_bar_popc(uint32_t id, uint32_t nthreads, bool pred) {
+  uint32_t c;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t"
+      "barrier.cta.red.popc.u32 %0, %1, %2, p;\n\t}"
+      : "=r"(c)
+      : "r"(id), "r"(nthreads), "r"(static_cast<uint32_t>(pred))
+      : "memory");
+  return c;
+}
 
 // ------------------------------------------- release/acquire (look-back)
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {

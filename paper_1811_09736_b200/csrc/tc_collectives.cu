@@ -92,6 +92,7 @@ constexpr int MODE_ROWS = 1;
 constexpr int MODE_TILES = 2;
 constexpr int MODE_GENERAL = 3;
 constexpr int MODE_CHUNK = 4;
+constexpr int MODE_IRREG = 5;  // irregular segments from a CSR offsets array
 constexpr int kMaxCtas = 1024;                    // persistent grid cap
 constexpr long long kScanPrepassMax = 1LL << 18;  // largest seg whose range-entry carry is recomputed
 constexpr unsigned kFull = 0xffffffffu;
@@ -135,6 +136,7 @@ struct Params {
   uint64_t* u_word;    // CHUNK: per-unit aggregate, one 64-bit word (see unit_word)
   int exclusive;
   int need_fixup;  // reduce: segments may straddle CTA ranges
+  const long long* offs;  // IRREG: nseg + 1 non-decreasing offsets, offs[0] = 0, offs[nseg] = n
 };
 
 template <typename T>
@@ -174,7 +176,9 @@ __host__ __device__ constexpr int pow2_at_least(int v) {
 template <int OP, int GR, int MODE, typename OutT>
 struct Cfg {
   static constexpr int G = 64 / GR;                                      // granule size
-  static constexpr int N = (OP == OP_SCAN) ? 64 : (GR < 16 ? 16 : GR);  // UMMA N
+  static constexpr bool IRREG = (MODE == MODE_IRREG);
+  // UMMA N: scans and IRREG take the full in-row prefix X.U (64 columns)
+  static constexpr int N = (OP == OP_SCAN || IRREG) ? 64 : (GR < 16 ? 16 : GR);
   static constexpr bool CHUNK = (MODE == MODE_CHUNK);
   // CTAs per SM (CHUNK keeps 2-4 units of tiles in TMEM: all 512 columns, 1 CTA/SM)
   // GENERAL reduce with 8..32 granules per row runs 3 CTAs/SM: its per-tile
@@ -203,7 +207,7 @@ struct Cfg {
   static constexpr uint32_t OFF_B = STAGES * kTileBytes;
   static constexpr uint32_t OFF_OUT = OFF_B + ((N * 128 + 1023) / 1024) * 1024;
   static constexpr uint32_t OFF_MISC = OFF_OUT + OUT_BUFS * OUT_BYTES;
-  static constexpr int LD_COLS = (OP == OP_SCAN) ? 64 : GR;  // TMEM columns read per tile
+  static constexpr int LD_COLS = (OP == OP_SCAN || IRREG) ? 64 : GR;  // TMEM columns read per tile
   static constexpr bool CONTIG = (MODE != MODE_CHUNK);       // contiguous CTA tile ranges
 };
 
@@ -228,6 +232,10 @@ struct Misc {
   float apv[2][4];  // aggregate warps' exchange
   int apf[2][4];
   double apd[2][4];
+  int icnt[2][kTileRows];  // IRREG: segment starts per row of the tile (double-buffered)
+  int iwt[2][4];           // IRREG: per-warp start counts
+  double idv[4];           // IRREG scan: carry-in composition scratch
+  int idf[4];
   uint64_t pfull[4];   // CHUNK: prefix warp -> epilogue (entry value of unit j ready)
   uint64_t pempty[4];  // CHUNK: epilogue -> prefix warp (slot consumed)
   double entry[4];
@@ -499,6 +507,124 @@ __device__ __forceinline__ void store_run(OutT* out, long long q0, const float (
     if (q0 + j <= qlast) out[q0 + j] = cvt_out<OutT>(v[j]);
 }
 
+// IRREG: P(b) = sum of the first b elements of a row (b in [0, 64]), read
+// from the row's in-row inclusive prefix v = (X.U)[row] at a per-thread
+// position: a 6-level select tree over registers (no local-memory indexing).
+__device__ __forceinline__ float row_prefix(const float (&v)[64], int b) {
+  const int i = b - 1;  // v[i] = sum of elements 0..i
+  float a[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) a[j] = (i & 32) ? v[j + 32] : v[j];
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+#pragma unroll
+    for (int j = 0; j < w; ++j) a[j] = (i & w) ? a[j + w] : a[j];
+  }
+  return b <= 0 ? 0.f : a[0];
+}
+
+// IRREG: first k in [0, nseg] with offs[k] >= v (offs[nseg] = n).
+__device__ __forceinline__ long long offs_lower_bound(const long long* offs, long long nseg,
+                                                      long long v) {
+  long long lo = 0, hi = nseg + 1;
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if (__ldg(offs + mid) < v)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// IRREG: contiguous tile range of CTA c (the main kernel's CONTIG split).
+__device__ __forceinline__ void irreg_range(long long T, int c, int G, long long n, long long* rb,
+                                            long long* re) {
+  const long long tb = T * c / G, te = T * (c + 1) / G;
+  *rb = tb * kTileElems;
+  *re = te * kTileElems < n ? te * kTileElems : n;
+}
+
+// IRREG scan, pass 1 ("range tails"): for CTA range c of the main kernel,
+// the value the open segment carries OUT of the range -- the sum from the
+// range's last segment start (flag 1), or of the whole range when no
+// segment starts in it (flag 0).  Reads only those tails: sum over ranges
+// of (range end - last start) <= n, typically a few segments per range.
+// Deterministic (fixed per-thread assignment, fixed fp64 tree).
+__global__ void __launch_bounds__(256) irreg_tail_kernel(const __half* x, int in_bf16, long long n,
+                                                         const long long* offs, long long nseg,
+                                                         long long T, Entry* tails) {
+  const int c = blockIdx.x;
+  long long rb, re;
+  irreg_range(T, c, gridDim.x, n, &rb, &re);
+  __shared__ long long s_lo;
+  __shared__ int s_flag;
+  __shared__ double s_part[8];
+  if (threadIdx.x == 0) {
+    long long lo = rb;
+    int flag = 0;
+    if (re > rb) {
+      // last real start (k < nseg) below re
+      const long long k = offs_lower_bound(offs, nseg, re) - 1;
+      if (k >= 0 && k < nseg && __ldg(offs + k) >= rb) {
+        lo = __ldg(offs + k);
+        flag = 1;
+      }
+    }
+    s_lo = lo;
+    s_flag = flag;
+  }
+  __syncthreads();
+  const long long lo = s_lo;
+  const bool bf16 = in_bf16 != 0;
+  double acc = 0.0;
+  if (re > lo) {
+    long long a = (lo + 7) & ~7LL;
+    if (a > re) a = re;
+    if (threadIdx.x == 0)
+      for (long long e = lo; e < a; ++e) acc += in_to_float(x, e, bf16);
+    const long long nb = (re - a) >> 3;
+    const uint4* xv = reinterpret_cast<const uint4*>(x + a);
+    float fs = 0.f;
+    int cnt = 0;
+    for (long long b = threadIdx.x; b < nb; b += blockDim.x) {
+      const uint4 w = __ldg(xv + b);
+      if (bf16) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f2 = __bfloat1622float2(h[k]);
+          fs += f2.x + f2.y;
+        }
+      } else {
+        const __half2* h = reinterpret_cast<const __half2*>(&w);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f2 = __half22float2(h[k]);
+          fs += f2.x + f2.y;
+        }
+      }
+      if (++cnt == 64) {
+        acc += fs;
+        fs = 0.f;
+        cnt = 0;
+      }
+    }
+    acc += fs;
+    if (threadIdx.x == blockDim.x - 1)
+      for (long long e = a + nb * 8; e < re; ++e) acc += in_to_float(x, e, bf16);
+  }
+  acc = warp_sum_d(acc);
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += s_part[w];
+    tails[c].seg = s_flag;
+    tails[c].val = t;
+  }
+}
+
 template <int OP, int GR, int MODE, typename OutT>
 __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, GR, MODE, OutT>::MINB))
     seg_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
@@ -592,7 +718,10 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
     ptx::tmem_alloc(&misc->tmem_base, C::TMEM_COLS);
     ptx::tmem_relinquish();
   }
-  build_b<OP, GR, N>(smem + C::OFF_B, p.in_bf16 ? 0x3F80 : 0x3C00);
+  build_b<(C::IRREG ? OP_SCAN : OP), GR, N>(smem + C::OFF_B, p.in_bf16 ? 0x3F80 : 0x3C00);
+  if constexpr (C::IRREG) {
+    for (int k = threadIdx.x; k < 2 * kTileRows; k += blockDim.x) (&misc->icnt[0][0])[k] = 0;
+  }
   ptx::fence_proxy_async_smem();  // B written by the generic proxy, read by the tensor core
   ptx::tc_fence_before();
   __syncthreads();
@@ -668,6 +797,106 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
       carry = epi_range_sum(p.x, p.in_bf16 != 0, seg_start, range_first_elem, et, lane, qd, misc);
       if (seg_start == 0 && has_carry) carry += *p.carry_in;
     }
+
+    // IRREG: kc = first offsets index whose start is at or after the current
+    // tile (= lower_bound(offs, tile base)); krange0 = the same at the range
+    // start (segments below it began in an earlier CTA's range)
+    long long kc = 0, krange0 = 0;
+    if constexpr (C::IRREG) {
+      kc = offs_lower_bound(p.offs, p.nseg, range_first_elem);
+      krange0 = kc;
+      if constexpr (OP == OP_SCAN) {
+        // value carried into this range: compose pass 1's range tails of the
+        // CTAs below, (value, has-start) in CTA order -- the sum of the tails
+        // from the last range holding a start on
+        const Entry* tails = p.entries;
+        int lf = -1;
+        for (int c2 = et; c2 < cta; c2 += kEpiThreads)
+          if (__ldcg(&tails[c2].seg)) lf = c2;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const int y = __shfl_xor_sync(kFull, lf, o);
+          lf = y > lf ? y : lf;
+        }
+        if (lane == 0) misc->idf[qd] = lf;
+        ptx::named_bar_sync(kEpiBar, kEpiThreads);
+        int lfa = misc->idf[0];
+#pragma unroll
+        for (int k = 1; k < 4; ++k) lfa = misc->idf[k] > lfa ? misc->idf[k] : lfa;
+        double acc = 0.0;
+        for (int c2 = et; c2 < cta; c2 += kEpiThreads)
+          if (c2 >= lfa) acc += __ldcg(&tails[c2].val);
+        acc = warp_sum_d(acc);
+        if (lane == 0) misc->idv[qd] = acc;
+        ptx::named_bar_sync(kEpiBar, kEpiThreads);
+        carry = (misc->idv[0] + misc->idv[1]) + (misc->idv[2] + misc->idv[3]);
+      }
+    }
+    // IRREG: the starts [lo, hi) of this thread's row in tile t.  Pass A
+    // counts the tile's starts per row (smem atomics; the count of starts
+    // below the tile end comes back through the barrier's popc, 128 offsets
+    // per round), then an exclusive scan of the per-row counts places each
+    // row's range.  The global last tile also takes the starts at n (empty
+    // trailing segments, and the end offset itself) into its last row.
+    auto irreg_rows = [&](long long t, int par, long long& lo, long long& hi) {
+      const long long tb = t * kTileElems;
+      const long long te = (t == T - 1) ? (1LL << 62) : tb + kTileElems;
+      int* cnt = misc->icnt[par];
+      long long kb = kc;
+      for (;;) {
+        const long long k = kb + et;
+        bool in = false;
+        if (k <= p.nseg) {
+          const long long o = __ldg(p.offs + k);
+          in = o < te;
+          if (in) {
+            long long rr = (o - tb) >> 6;
+            rr = rr < 0 ? 0 : (rr > kTileRows - 1 ? kTileRows - 1 : rr);
+            atomicAdd(&cnt[rr], 1);
+          }
+        }
+        const int c = static_cast<int>(ptx::named_bar_popc(kEpiBar, kEpiThreads, in));
+        kb += c;
+        if (c < kEpiThreads) break;
+      }
+      const int cr = cnt[rit];
+      cnt[rit] = 0;  // reset for the tile after next (same buffer)
+      int incl = cr;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int u = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) incl += u;
+      }
+      if (lane == 31) misc->iwt[par][qd] = incl;
+      ptx::named_bar_sync(kEpiBar, kEpiThreads);
+      int woff = 0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        if (k < qd) woff += misc->iwt[par][k];
+      lo = kc + woff + (incl - cr);
+      hi = lo + cr;
+      kc = kb;
+    };
+    // IRREG: the row's in-row inclusive prefix from TMEM; the ragged last
+    // row (outside the TMA view) is recomputed from HBM
+    auto irreg_load_row = [&](const auto& r, long long row, float (&vv)[64]) {
+#pragma unroll
+      for (int k = 0; k < 64; ++k) vv[k] = __uint_as_float(r[k]);
+      if (row == p.rows_full) {
+        float s = 0.f;
+#pragma unroll
+        for (int k = 0; k < 64; ++k) {
+          const long long e = row * kRow + k;
+          s += (e < p.n) ? in_to_float(p.x, e, p.in_bf16 != 0) : 0.f;
+          vv[k] = s;
+        }
+      }
+    };
+    // position of an offset inside the row, clamped to [0, 64] (memory safety
+    // for malformed offsets; exact for valid ones)
+    auto irreg_pos = [](long long b) -> int {
+      return static_cast<int>(b < 0 ? 0 : (b > kRow ? kRow : b));
+    };
 
     // CHUNK: aggregate of the unit being reduced (P1), and of the last two
     // units, kept until their P2 (one-unit lag)
@@ -871,6 +1100,10 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
         if constexpr (!C::CONTIG) {
           q0 = (t * kTileRows + rit) * GR;
         }
+        // IRREG: segment starts of this row, [i_lo, i_hi) in offs (before the
+        // TMEM wait, so the offset loads overlap the MMA)
+        long long i_lo = 0, i_hi = 0;
+        if constexpr (C::IRREG) irreg_rows(t, par, i_lo, i_hi);
         if (wait_full) ptx::mbar_wait_warp(&misc->tfull[a], aph);
         ptx::tc_fence_after();
         constexpr int LD = C::LD_COLS;
@@ -891,7 +1124,63 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
 
         const long long row = t * kTileRows + rit;
 
-        if constexpr (OP == OP_REDUCE) {
+        if constexpr (C::IRREG && OP == OP_REDUCE) {
+          // ================================================= irregular reduce
+          // row pieces from the in-row prefix P (X.U): segment k starting in
+          // this row is complete here iff the next start is in this row too;
+          // the row's first start closes segment i_lo - 1 (head = P(start))
+          float vv[64];
+          irreg_load_row(r, row, vv);
+          OutT* out = reinterpret_cast<OutT*>(p.out);
+          const long long rowbase = row * kRow;
+          const int seen = (i_hi > i_lo) ? 1 : 0;
+          float head = 0.f, run = vv[63];
+          if (seen) {
+            float pb = row_prefix(vv, irreg_pos(__ldg(p.offs + i_lo) - rowbase));
+            head = pb;
+            for (long long k = i_lo; k + 1 < i_hi; ++k) {
+              const float p2 = row_prefix(vv, irreg_pos(__ldg(p.offs + k + 1) - rowbase));
+              out[k] = cvt_out<OutT>(p2 - pb);
+              pb = p2;
+            }
+            run = vv[63] - pb;
+          }
+          float v = run;
+          int f = seen;
+          warp_pair_scan(v, f, lane);
+          float ve = __shfl_up_sync(kFull, v, 1);
+          int fe = __shfl_up_sync(kFull, f, 1);
+          if (lane == 0) {
+            ve = 0.f;
+            fe = 0;
+          }
+          if (lane == 31) {
+            misc->pv[par][qd] = v;
+            misc->pf[par][qd] = f;
+          }
+          ptx::named_bar_sync(kEpiBar, kEpiThreads);
+          float wv = 0.f, tv = 0.f;
+          int wf = 0, tf = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float yv = misc->pv[par][k];
+            const int yf = misc->pf[par][k];
+            if (k < qd) compose(wv, wf, yv, yf);
+            compose(tv, tf, yv, yf);
+          }
+          compose(wv, wf, ve, fe);
+          const long long seg0 = i_lo - 1;
+          if (seen && seg0 >= 0) {
+            const double val = static_cast<double>(wv + head) + (wf ? 0.0 : carry);
+            if (seg0 < krange0) {
+              misc->head_seg = seg0;  // partial: segment began in an earlier CTA's range
+              misc->head_val = val;
+            } else {
+              out[seg0] = cvt_out_d<OutT>(val);
+            }
+          }
+          carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
+        } else if constexpr (OP == OP_REDUCE) {
           // ================================================= reduce
           float gs[GR];
   #pragma unroll
@@ -1106,6 +1395,58 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
               tpos = 0;
               ++tseg;
             }
+          } else if constexpr (C::IRREG) {
+            // irregular segments: starts of this row as a 64-bit mask; the
+            // row's (value, has-start) pair joins the same row/warp/tile
+            // pair scan, then each output is the in-row prefix minus P(the
+            // latest start at or before it), or plus the entering carry
+            const long long rowbase = row * kRow;
+            uint64_t msk = 0;
+            for (long long k = i_lo; k < i_hi && k < p.nseg; ++k) {
+              const long long b = __ldg(p.offs + k) - rowbase;
+              if (b >= 0 && b < kRow) msk |= 1ull << b;
+            }
+            float v = vv[63];
+            int f = msk != 0;
+            if (f) v = vv[63] - row_prefix(vv, 63 - __clzll(static_cast<long long>(msk)));
+            warp_pair_scan(v, f, lane);
+            float ve = __shfl_up_sync(kFull, v, 1);
+            int fe = __shfl_up_sync(kFull, f, 1);
+            if (lane == 0) {
+              ve = 0.f;
+              fe = 0;
+            }
+            if (lane == 31) {
+              misc->pv[par][qd] = v;
+              misc->pf[par][qd] = f;
+            }
+            ptx::named_bar_sync(kEpiBar, kEpiThreads);
+            float wv = 0.f, tv = 0.f;
+            int wf = 0, tf = 0;
+  #pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float yv = misc->pv[par][k];
+              const int yf = misc->pf[par][k];
+              if (k < qd) compose(wv, wf, yv, yf);
+              compose(tv, tf, yv, yf);
+            }
+            compose(wv, wf, ve, fe);
+            const double tprefix = carry;
+            carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
+            const float cinf = wf ? wv : static_cast<float>(tprefix + static_cast<double>(wv));
+            // final values in place, in element order (sub = P(latest start))
+            float sub = -cinf, prev = 0.f;
+            const bool excl = p.exclusive != 0;
+            const uint32_t mlo = static_cast<uint32_t>(msk), mhi = static_cast<uint32_t>(msk >> 32);
+  #pragma unroll
+            for (int e = 0; e < 64; ++e) {
+              const float cur = vv[e];
+              const bool st = ((e < 32 ? mlo : mhi) >> (e & 31)) & 1u;
+              if (st) sub = prev;
+              vv[e] = excl ? (st ? 0.f : prev - sub) : cur - sub;
+              prev = cur;
+            }
+            off[0] = 0.f;
           } else {
             // MODE_GENERAL / MODE_CHUNK: pair scan with granule starts
             if constexpr (MODE == MODE_CHUNK) {
@@ -1202,11 +1543,12 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
           constexpr bool ONE_OFF = (MODE == MODE_ROWS || MODE == MODE_TILES);
           const bool excl = p.exclusive != 0;
           auto outv = [&](int e) -> float {
+            if constexpr (C::IRREG) return vv[e];  // already final
             const float base = off[ONE_OFF ? 0 : e / G];
             if (excl) return (e % G == 0) ? (base + 0.f) : (vv[e - 1] + base);
             return vv[e] + base;
           };
-          if (p.total_out && row == (p.n - 1) / kRow) {
+          if (!C::IRREG && p.total_out && row == (p.n - 1) / kRow) {
             const int k = static_cast<int>((p.n - 1) % kRow);
             float incl = 0.f;
   #pragma unroll
@@ -1277,11 +1619,19 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
       if (leader) {
         if constexpr (OP == OP_REDUCE) {
           // open segment at the end of the range -> tail partial
-          const long long lg_end = t_end * static_cast<long long>(kTileRows) * GR;
-          const long long lg = (lg_end < p.qlast + 1 ? lg_end : p.qlast + 1) - 1;
-          const bool closed = ((lg + 1) % p.m == 0) || (lg == p.qlast);
           Entry e0{misc->head_seg, misc->head_val};
-          Entry e1{closed ? -1LL : lg / p.m, carry};
+          Entry e1{-1LL, carry};
+          if constexpr (C::IRREG) {
+            // kc - 1 = the last start before the range end; it is never
+            // closed inside the range (the row holding its end offset
+            // closes it), and it is the end offset itself in the last range
+            e1.seg = (kc - 1 < p.nseg) ? kc - 1 : -1LL;
+          } else {
+            const long long lg_end = t_end * static_cast<long long>(kTileRows) * GR;
+            const long long lg = (lg_end < p.qlast + 1 ? lg_end : p.qlast + 1) - 1;
+            const bool closed = ((lg + 1) % p.m == 0) || (lg == p.qlast);
+            e1.seg = closed ? -1LL : lg / p.m;
+          }
           p.entries[2 * cta] = e0;
           p.entries[2 * cta + 1] = e1;
         }
@@ -1654,6 +2004,17 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
+  if (MODE == MODE_IRREG && OP == OP_SCAN) {
+    // pass 1: the carry each CTA range hands on (same range split as below)
+    irreg_tail_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(p.x, p.in_bf16, p.n, p.offs,
+                                                                  p.nseg, p.num_tiles, p.entries);
+    const cudaError_t e1 = cudaGetLastError();
+    if (e1 != cudaSuccess) {
+      set_err("kernel launch failed: %s%lld", cudaGetErrorString(e1), 0);
+      return TC_CUDA_ERROR;
+    }
+    ++g_launches;
+  }
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tin, tout, p);
   if (e != cudaSuccess) {
     set_err("kernel launch failed: %s%lld", cudaGetErrorString(e), 0);
@@ -1689,6 +2050,7 @@ static LaunchFn pick(int gr, int mode) {
     case MODE_CHUNK:
       if constexpr (OP == OP_SCAN) return pick_gr<OP, MODE_CHUNK, OutT>(gr);
       return nullptr;
+    case MODE_IRREG: return gr == 1 ? &launch<OP, 1, MODE_IRREG, OutT> : nullptr;
   }
   return nullptr;
 }
@@ -1871,6 +2233,64 @@ int tc_full_scan(const void* x, int64_t n, void* out, int out_dtype, int exclusi
                      ws_bytes, stream);
 }
 
+// Irregular (CSR-offset) segments: validation shared by reduce and scan.
+static int irreg_checks(const void* x, int in_dtype, int64_t n, const int64_t* offsets,
+                        int64_t nseg, const void* out, int out_dtype, bool scan, void* ws,
+                        size_t ws_bytes) {
+  g_err[0] = 0;
+  int rc = common_checks(x, n, 1, out, out_dtype, scan, ws, ws_bytes,
+                         scan ? TC_OP_SCAN : TC_OP_REDUCE);
+  if (rc) return rc;
+  if (in_dtype != TC_F16 && in_dtype != TC_BF16) {
+    set_err("unsupported input dtype %s%lld", "", in_dtype);
+    return TC_BAD_CONFIG;
+  }
+  if (nseg < 1 || nseg > n + (1LL << 31)) {
+    set_err("segment count %s%lld outside [1, n + 2^31]", "", nseg);
+    return TC_BAD_LENGTH;
+  }
+  if (!offsets || (reinterpret_cast<uintptr_t>(offsets) & 7)) {
+    set_err("offsets must be a non-null, 8-byte aligned device pointer%s%lld", "", 0);
+    return TC_BAD_ALIGNMENT;
+  }
+  return TC_OK;
+}
+
+static Params irreg_params(const void* x, int in_dtype, int64_t n, const int64_t* offsets,
+                           int64_t nseg, void* out, void* ws, int op) {
+  int gr = 0, mode = 0;
+  Params p = make_params(x, n, n, out, ws, op, false, &gr, &mode);
+  p.in_bf16 = (in_dtype == TC_BF16) ? 1 : 0;
+  p.offs = reinterpret_cast<const long long*>(offsets);
+  p.nseg = nseg;
+  p.need_fixup = (op == TC_OP_REDUCE) ? 1 : 0;
+  return p;
+}
+
+int tc_irreg_reduce(const void* x, int in_dtype, int64_t n, const int64_t* offsets, int64_t nseg,
+                    void* out, int out_dtype, void* ws, size_t ws_bytes, void* stream) {
+  int rc = irreg_checks(x, in_dtype, n, offsets, nseg, out, out_dtype, false, ws, ws_bytes);
+  if (rc) return rc;
+  Params p = irreg_params(x, in_dtype, n, offsets, nseg, out, ws, TC_OP_REDUCE);
+  LaunchFn fn = (out_dtype == TC_F16)   ? pick<OP_REDUCE, __half>(1, MODE_IRREG)
+                : (out_dtype == TC_F32) ? pick<OP_REDUCE, float>(1, MODE_IRREG)
+                                        : pick<OP_REDUCE, double>(1, MODE_IRREG);
+  const int es = (out_dtype == TC_F16) ? 2 : (out_dtype == TC_F32) ? 4 : 8;
+  return fn(p, es, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int tc_irreg_scan(const void* x, int in_dtype, int64_t n, const int64_t* offsets, int64_t nseg,
+                  void* out, int out_dtype, int exclusive, void* ws, size_t ws_bytes,
+                  void* stream) {
+  int rc = irreg_checks(x, in_dtype, n, offsets, nseg, out, out_dtype, true, ws, ws_bytes);
+  if (rc) return rc;
+  Params p = irreg_params(x, in_dtype, n, offsets, nseg, out, ws, TC_OP_SCAN);
+  p.exclusive = exclusive ? 1 : 0;
+  LaunchFn fn = (out_dtype == TC_F16) ? pick<OP_SCAN, __half>(1, MODE_IRREG)
+                                      : pick<OP_SCAN, float>(1, MODE_IRREG);
+  return fn(p, out_dtype == TC_F16 ? 2 : 4, reinterpret_cast<cudaStream_t>(stream));
+}
+
 const char* tc_status_string(int s) {
   switch (s) {
     case TC_OK: return "ok";
@@ -1889,6 +2309,6 @@ const char* tc_last_error(void) { return g_err; }
 uint64_t tc_launch_count(void) { return g_launches; }
 void tc_reset_launch_count(void) { g_launches = 0; }
 
-int tc_abi_version(void) { return (1 << 16) | 1; }
+int tc_abi_version(void) { return (1 << 16) | 2; }
 
 }  // extern "C"

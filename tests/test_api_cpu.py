@@ -188,3 +188,41 @@ def test_oracle_is_not_imported_by_the_product():
     for p in (ROOT / "paper_1811_09736_b200").rglob("*.py"):
         src = p.read_text()
         assert "import oracle" not in src and "from oracle" not in src, p
+
+
+def test_irregular_validation_before_device():
+    """Irregular (CSR-offset) entry points: offset errors raise before any
+    device work; the C ABI rejects bad counts / pointers with status codes."""
+    x = np.ones(100, np.float16)
+    for bad in ([0, 50, 40, 100], [1, 100], [0, 99], [[0, 100]]):
+        exc = BadLengthError if np.ndim(bad) != 1 else BadConfigError
+        with pytest.raises(exc):
+            ht.irregular_segmented_reduce(x, bad)
+        with pytest.raises(exc):
+            ht.irregular_segmented_scan(x, bad)
+    with pytest.raises(BadLengthError):
+        ht.irregular_segmented_reduce(x, [0])
+    with pytest.raises(BadLengthError):
+        ht.irregular_segmented_reduce(np.ones(0, np.float16), [0, 0])
+    L = _lib.lib
+    ws = ctypes.create_string_buffer(1 << 16)
+    wsp = (ctypes.addressof(ws) + 255) & ~255
+    xp, out, offp = 1 << 20, 2 << 20, 3 << 20
+    assert L.tc_irreg_reduce(xp, 0, 100, offp, 0, out, _lib.TC_F32, wsp, 60000, None) == _lib.TC_BAD_LENGTH
+    assert L.tc_irreg_reduce(xp, 0, 100, offp + 4, 3, out, _lib.TC_F32, wsp, 60000,
+                             None) == _lib.TC_BAD_ALIGNMENT
+    assert L.tc_irreg_reduce(xp, 0, 100, None, 3, out, _lib.TC_F32, wsp, 60000, None) == _lib.TC_BAD_ALIGNMENT
+    assert L.tc_irreg_reduce(xp, 7, 100, offp, 3, out, _lib.TC_F32, wsp, 60000, None) == _lib.TC_BAD_CONFIG
+    assert L.tc_irreg_scan(xp, 0, 100, offp, 3, out, _lib.TC_F64, 0, wsp, 60000, None) == _lib.TC_BAD_CONFIG
+    assert L.tc_irreg_scan(xp, 0, 0, offp, 3, out, _lib.TC_F32, 0, wsp, 60000, None) == _lib.TC_BAD_LENGTH
+
+
+def test_irregular_no_cpu_fallback():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible; covered by the gpu suite")
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        ht.irregular_segmented_reduce(np.ones(64, np.float16), [0, 10, 64])
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        ht.irregular_segmented_scan(np.ones(64, np.float16), [0, 10, 64])

@@ -167,3 +167,25 @@ def test_c_oracle_matches_numpy(liboracle, rng, n, s):
                 liboracle.or_seg_scan(x.ctypes.data, n, s, inc, c, hc, o.ctypes.data, 8)
                 r = O.ref_seg_scan(x, s, bool(inc), c if hc else None)
                 assert np.array_equal(o, r) if kind == "int" else np.allclose(o, r, rtol=1e-13)
+
+
+def test_irregular_oracle_against_direct_loops():
+    """The irregular oracle (extension, no reference fixture exists: the
+    paper elides irregular segments) against per-segment
+    binary64 loops -- the definition restated directly."""
+    rng = np.random.default_rng(3)
+    for n, mean, ef in ((1, 1, 0.0), (1000, 1, 0.5), (5000, 37, 0.2), (20000, 3000, 0.0)):
+        x = rng.random(n).astype(np.float16)
+        off = O.random_offsets(rng, n, mean, ef)
+        assert off[0] == 0 and off[-1] == n and np.all(np.diff(off) >= 0)
+        xs = x.astype(np.float64)
+        r = O.ref_irreg_reduce(x, off)
+        s = O.ref_irreg_scan(x, off)
+        e = O.ref_irreg_scan(x, off, inclusive=False)
+        for k in range(off.size - 1):
+            a, b = off[k], off[k + 1]
+            assert r[k] == pytest.approx(xs[a:b].sum(), rel=1e-15, abs=0)
+            c = np.cumsum(xs[a:b])
+            assert np.allclose(s[a:b], c, rtol=1e-14, atol=0)
+            if b > a:
+                assert e[a] == 0 and np.allclose(e[a + 1:b], c[:-1], rtol=1e-14, atol=0)
