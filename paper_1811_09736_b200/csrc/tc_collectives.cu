@@ -233,7 +233,6 @@ struct Misc {
   int apf[2][4];
   double apd[2][4];
   int icnt[2][kTileRows];  // IRREG: segment starts per row of the tile (double-buffered)
-  int iwt[2][4];           // IRREG: per-warp start counts
   double idv[4];           // IRREG scan: carry-in composition scratch
   int idf[4];
   uint64_t pfull[4];   // CHUNK: prefix warp -> epilogue (entry value of unit j ready)
@@ -551,7 +550,8 @@ __device__ __forceinline__ void irreg_range(long long T, int c, int G, long long
 // segment starts in it (flag 0).  Reads only those tails: sum over ranges
 // of (range end - last start) <= n, typically a few segments per range.
 // Deterministic (fixed per-thread assignment, fixed fp64 tree).
-__global__ void __launch_bounds__(256) irreg_tail_kernel(const __half* x, int in_bf16, long long n,
+constexpr int kTailThreads = 512;
+__global__ void __launch_bounds__(kTailThreads) irreg_tail_kernel(const __half* x, int in_bf16, long long n,
                                                          const long long* offs, long long nseg,
                                                          long long T, Entry* tails) {
   const int c = blockIdx.x;
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(256) irreg_tail_kernel(const __half* x, int in
   irreg_range(T, c, gridDim.x, n, &rb, &re);
   __shared__ long long s_lo;
   __shared__ int s_flag;
-  __shared__ double s_part[8];
+  __shared__ double s_part[kTailThreads / 32];
   if (threadIdx.x == 0) {
     long long lo = rb;
     int flag = 0;
@@ -585,10 +585,8 @@ __global__ void __launch_bounds__(256) irreg_tail_kernel(const __half* x, int in
       for (long long e = lo; e < a; ++e) acc += in_to_float(x, e, bf16);
     const long long nb = (re - a) >> 3;
     const uint4* xv = reinterpret_cast<const uint4*>(x + a);
-    float fs = 0.f;
-    int cnt = 0;
-    for (long long b = threadIdx.x; b < nb; b += blockDim.x) {
-      const uint4 w = __ldg(xv + b);
+    constexpr int U = 4;  // independent 16-B loads in flight per thread
+    auto add8 = [&](const uint4& w, float& fs) {
       if (bf16) {
         const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
 #pragma unroll
@@ -604,13 +602,23 @@ __global__ void __launch_bounds__(256) irreg_tail_kernel(const __half* x, int in
           fs += f2.x + f2.y;
         }
       }
-      if (++cnt == 64) {
-        acc += fs;
-        fs = 0.f;
-        cnt = 0;
-      }
+    };
+    const long long step = static_cast<long long>(blockDim.x) * U;
+    long long b = threadIdx.x;
+    for (; b + (U - 1) * blockDim.x < nb; b += step) {  // <= 512 elements per thread per fp32 partial
+      uint4 w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) w[u] = __ldcs(xv + b + u * blockDim.x);
+      float fs = 0.f;
+#pragma unroll
+      for (int u = 0; u < U; ++u) add8(w[u], fs);
+      acc += fs;
     }
-    acc += fs;
+    for (; b < nb; b += blockDim.x) {
+      float fs = 0.f;
+      add8(__ldcs(xv + b), fs);
+      acc += fs;
+    }
     if (threadIdx.x == blockDim.x - 1)
       for (long long e = a + nb * 8; e < re; ++e) acc += in_to_float(x, e, bf16);
   }
@@ -619,7 +627,7 @@ __global__ void __launch_bounds__(256) irreg_tail_kernel(const __half* x, int in
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int w = 0; w < 8; ++w) t += s_part[w];
+    for (int w = 0; w < kTailThreads / 32; ++w) t += s_part[w];
     tails[c].seg = s_flag;
     tails[c].val = t;
   }
@@ -803,7 +811,29 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
     // start (segments below it began in an earlier CTA's range)
     long long kc = 0, krange0 = 0;
     if constexpr (C::IRREG) {
-      kc = offs_lower_bound(p.offs, p.nseg, range_first_elem);
+      {
+        // 128-ary search by the epilogue threads: ~4 dependent rounds
+        // instead of log2(nseg) serial loads; answer in [lo, hi], offs[hi] >= v
+        const long long v = range_first_elem;
+        long long lo = 0, hi = p.nseg;
+        while (hi - lo > kEpiThreads) {
+          const long long span = hi - lo;
+          const long long q = lo + span * et / kEpiThreads;  // increasing in et; et = 0 unprobed
+          const bool below = et > 0 && __ldg(p.offs + q) < v;
+          const long long c = ptx::named_bar_popc(kEpiBar, kEpiThreads, below);
+          const long long lo0 = lo;
+          if (c > 0) lo = lo0 + span * c / kEpiThreads + 1;  // probes 1..c are below v
+          hi = lo0 + span * (c + 1) / kEpiThreads;           // probe c + 1 (c = 127: hi)
+        }
+        while (lo < hi) {
+          const long long mid = (lo + hi) >> 1;
+          if (__ldg(p.offs + mid) < v)
+            lo = mid + 1;
+          else
+            hi = mid;
+        }
+        kc = lo;
+      }
       krange0 = kc;
       if constexpr (OP == OP_SCAN) {
         // value carried into this range: compose pass 1's range tails of the
@@ -838,44 +868,70 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
     // per round), then an exclusive scan of the per-row counts places each
     // row's range.  The global last tile also takes the starts at n (empty
     // trailing segments, and the end offset itself) into its last row.
-    auto irreg_rows = [&](long long t, int par, long long& lo, long long& hi) {
+    // The first two rounds of the next tile's offsets are prefetched into
+    // registers at the end of this tile's pass A, so their (HBM / L2)
+    // latency overlaps this tile's epilogue.
+    constexpr long long kNoStart = 1LL << 62;
+    long long pf0 = kNoStart, pf1 = kNoStart;
+    bool pf_ok = false;
+    auto ld_off = [&](long long k) -> long long {
+      return k <= p.nseg ? __ldg(p.offs + k) : kNoStart;
+    };
+    auto irreg_rows = [&](long long t, int par, long long& lo, long long& hi) -> long long {
       const long long tb = t * kTileElems;
-      const long long te = (t == T - 1) ? (1LL << 62) : tb + kTileElems;
+      const long long te = (t == T - 1) ? kNoStart - 1 : tb + kTileElems;
       int* cnt = misc->icnt[par];
+      // the previous tile's counts (other buffer) were read by everyone
+      // before that tile's pair-scan barrier: clear this thread's row
+      misc->icnt[par ^ 1][rit] = 0;
       long long kb = kc;
-      for (;;) {
-        const long long k = kb + et;
-        bool in = false;
-        if (k <= p.nseg) {
-          const long long o = __ldg(p.offs + k);
-          in = o < te;
-          if (in) {
-            long long rr = (o - tb) >> 6;
-            rr = rr < 0 ? 0 : (rr > kTileRows - 1 ? kTileRows - 1 : rr);
-            atomicAdd(&cnt[rr], 1);
-          }
+      for (int round = 0;; ++round) {
+        const long long o = (pf_ok && round == 0) ? pf0
+                            : (pf_ok && round == 1) ? pf1
+                                                    : ld_off(kb + et);
+        const bool in = o < te;
+        if (in) {
+          long long rr = (o - tb) >> 6;
+          rr = rr < 0 ? 0 : (rr > kTileRows - 1 ? kTileRows - 1 : rr);
+          atomicAdd(&cnt[rr], 1);
         }
         const int c = static_cast<int>(ptx::named_bar_popc(kEpiBar, kEpiThreads, in));
         kb += c;
         if (c < kEpiThreads) break;
       }
+      pf0 = ld_off(kb + et);
+      pf1 = ld_off(kb + et + kEpiThreads);
+      pf_ok = true;
+      // and the next 2 KB of offsets into L2 (the array is consumed in order)
+      if (et < 16) {
+        const long long kp = kb + 2 * kEpiThreads + 16 * et;
+        if (kp <= p.nseg) ptx::prefetch_l2(p.offs + kp);
+      }
+      // the counts are complete (popc barrier): the exclusive prefix over
+      // rows = the warp's inclusive scan + the rows of the lower warps, read
+      // straight from smem (no further barrier)
+      const long long tile_starts = kb - kc;  // uniform
+      if (tile_starts == 0) {
+        lo = hi = kc;
+        return 0;
+      }
       const int cr = cnt[rit];
-      cnt[rit] = 0;  // reset for the tile after next (same buffer)
       int incl = cr;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const int u = __shfl_up_sync(kFull, incl, d);
         if (lane >= d) incl += u;
       }
-      if (lane == 31) misc->iwt[par][qd] = incl;
-      ptx::named_bar_sync(kEpiBar, kEpiThreads);
       int woff = 0;
 #pragma unroll
       for (int k = 0; k < 3; ++k)
-        if (k < qd) woff += misc->iwt[par][k];
+        if (k < qd) woff += cnt[32 * k + lane];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) woff += __shfl_xor_sync(kFull, woff, o);
       lo = kc + woff + (incl - cr);
       hi = lo + cr;
       kc = kb;
+      return tile_starts;
     };
     // IRREG: the row's in-row inclusive prefix from TMEM; the ragged last
     // row (outside the TMA view) is recomputed from HBM
@@ -1102,8 +1158,8 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
         }
         // IRREG: segment starts of this row, [i_lo, i_hi) in offs (before the
         // TMEM wait, so the offset loads overlap the MMA)
-        long long i_lo = 0, i_hi = 0;
-        if constexpr (C::IRREG) irreg_rows(t, par, i_lo, i_hi);
+        long long i_lo = 0, i_hi = 0, i_tn = 1;  // i_tn: segment starts in the tile (uniform)
+        if constexpr (C::IRREG) i_tn = irreg_rows(t, par, i_lo, i_hi);
         if (wait_full) ptx::mbar_wait_warp(&misc->tfull[a], aph);
         ptx::tc_fence_after();
         constexpr int LD = C::LD_COLS;
@@ -1131,6 +1187,15 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
           // the row's first start closes segment i_lo - 1 (head = P(start))
           float vv[64];
           irreg_load_row(r, row, vv);
+          if (i_tn == 0) {
+            // no segment starts in the tile: its sum joins the open segment
+            const float ws = warp_sum(vv[63]);
+            if (lane == 0) misc->pv[par][qd] = ws;
+            ptx::named_bar_sync(kEpiBar, kEpiThreads);
+            carry += static_cast<double>((misc->pv[par][0] + misc->pv[par][1]) +
+                                         (misc->pv[par][2] + misc->pv[par][3]));
+            return;
+          }
           OutT* out = reinterpret_cast<OutT*>(p.out);
           const long long rowbase = row * kRow;
           const int seen = (i_hi > i_lo) ? 1 : 0;
@@ -1402,49 +1467,76 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
             // latest start at or before it), or plus the entering carry
             const long long rowbase = row * kRow;
             uint64_t msk = 0;
-            for (long long k = i_lo; k < i_hi && k < p.nseg; ++k) {
-              const long long b = __ldg(p.offs + k) - rowbase;
-              if (b >= 0 && b < kRow) msk |= 1ull << b;
-            }
-            float v = vv[63];
-            int f = msk != 0;
-            if (f) v = vv[63] - row_prefix(vv, 63 - __clzll(static_cast<long long>(msk)));
-            warp_pair_scan(v, f, lane);
-            float ve = __shfl_up_sync(kFull, v, 1);
-            int fe = __shfl_up_sync(kFull, f, 1);
-            if (lane == 0) {
-              ve = 0.f;
-              fe = 0;
-            }
-            if (lane == 31) {
-              misc->pv[par][qd] = v;
-              misc->pf[par][qd] = f;
-            }
-            ptx::named_bar_sync(kEpiBar, kEpiThreads);
-            float wv = 0.f, tv = 0.f;
-            int wf = 0, tf = 0;
+            float cinf;  // value of the open segment entering the row
+            if (i_tn == 0) {
+              // no segment starts in the tile: a plain row scan
+              const float incl = warp_incl_scan(vv[63], lane);
+              float ex = __shfl_up_sync(kFull, incl, 1);
+              if (lane == 0) ex = 0.f;
+              if (lane == 31) misc->pv[par][qd] = incl;
+              ptx::named_bar_sync(kEpiBar, kEpiThreads);
+              float woff = 0.f, ttot = 0.f;
   #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float yv = misc->pv[par][k];
-              const int yf = misc->pf[par][k];
-              if (k < qd) compose(wv, wf, yv, yf);
-              compose(tv, tf, yv, yf);
+              for (int k = 0; k < 4; ++k) {
+                const float y = misc->pv[par][k];
+                if (k < qd) woff += y;
+                ttot += y;
+              }
+              cinf = static_cast<float>(carry + static_cast<double>(ex + woff));
+              carry += static_cast<double>(ttot);
+            } else {
+              for (long long k = i_lo; k < i_hi && k < p.nseg; ++k) {
+                const long long b = __ldg(p.offs + k) - rowbase;
+                if (b >= 0 && b < kRow) msk |= 1ull << b;
+              }
+              float v = vv[63];
+              int f = msk != 0;
+              if (f) v = vv[63] - row_prefix(vv, 63 - __clzll(static_cast<long long>(msk)));
+              warp_pair_scan(v, f, lane);
+              float ve = __shfl_up_sync(kFull, v, 1);
+              int fe = __shfl_up_sync(kFull, f, 1);
+              if (lane == 0) {
+                ve = 0.f;
+                fe = 0;
+              }
+              if (lane == 31) {
+                misc->pv[par][qd] = v;
+                misc->pf[par][qd] = f;
+              }
+              ptx::named_bar_sync(kEpiBar, kEpiThreads);
+              float wv = 0.f, tv = 0.f;
+              int wf = 0, tf = 0;
+  #pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const float yv = misc->pv[par][k];
+                const int yf = misc->pf[par][k];
+                if (k < qd) compose(wv, wf, yv, yf);
+                compose(tv, tf, yv, yf);
+              }
+              compose(wv, wf, ve, fe);
+              const double tprefix = carry;
+              carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
+              cinf = wf ? wv : static_cast<float>(tprefix + static_cast<double>(wv));
             }
-            compose(wv, wf, ve, fe);
-            const double tprefix = carry;
-            carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
-            const float cinf = wf ? wv : static_cast<float>(tprefix + static_cast<double>(wv));
             // final values in place, in element order (sub = P(latest start))
             float sub = -cinf, prev = 0.f;
             const bool excl = p.exclusive != 0;
             const uint32_t mlo = static_cast<uint32_t>(msk), mhi = static_cast<uint32_t>(msk >> 32);
+            if (__any_sync(kFull, msk != 0)) {
   #pragma unroll
-            for (int e = 0; e < 64; ++e) {
-              const float cur = vv[e];
-              const bool st = ((e < 32 ? mlo : mhi) >> (e & 31)) & 1u;
-              if (st) sub = prev;
-              vv[e] = excl ? (st ? 0.f : prev - sub) : cur - sub;
-              prev = cur;
+              for (int e = 0; e < 64; ++e) {
+                const float cur = vv[e];
+                const bool st = ((e < 32 ? mlo : mhi) >> (e & 31)) & 1u;
+                if (st) sub = prev;
+                vv[e] = excl ? (st ? 0.f : prev - sub) : cur - sub;
+                prev = cur;
+              }
+            } else if (excl) {
+  #pragma unroll
+              for (int e = 63; e >= 0; --e) vv[e] = (e ? vv[e - 1] : 0.f) + cinf;
+            } else {
+  #pragma unroll
+              for (int e = 0; e < 64; ++e) vv[e] += cinf;
             }
             off[0] = 0.f;
           } else {
@@ -1940,7 +2032,7 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
   // 97 %, fp16 scans 93-95 vs 91-92 %); cooperative launches (CHUNK) must
   // match the API.
   if (MODE != MODE_CHUNK) {
-    per_sm = (MODE == MODE_GENERAL) ? Cfg<OP, GR, MODE, OutT>::MINB
+    per_sm = (MODE == MODE_GENERAL || MODE == MODE_IRREG) ? Cfg<OP, GR, MODE, OutT>::MINB
              : ((OP == OP_REDUCE && MODE == MODE_ROWS && p0.log2m >= 4) ||
                 (OP == OP_SCAN && MODE == MODE_LOCAL && sizeof(OutT) == 4))
                  ? 2
@@ -2006,7 +2098,7 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
   cfg.numAttrs = na;
   if (MODE == MODE_IRREG && OP == OP_SCAN) {
     // pass 1: the carry each CTA range hands on (same range split as below)
-    irreg_tail_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(p.x, p.in_bf16, p.n, p.offs,
+    irreg_tail_kernel<<<static_cast<unsigned>(grid), kTailThreads, 0, st>>>(p.x, p.in_bf16, p.n, p.offs,
                                                                   p.nseg, p.num_tiles, p.entries);
     const cudaError_t e1 = cudaGetLastError();
     if (e1 != cudaSuccess) {
