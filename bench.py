@@ -240,6 +240,21 @@ def gen_device(n, device, seed):
     return x
 
 
+def irregular_offsets(n, mean, device, seed):
+    """int64 CSR offsets over [0, n] with geometric segment lengths (mean `mean`)."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    m = int(2 * n / mean) + 16
+    u = torch.rand(m, device=device, generator=g, dtype=torch.float64).clamp_min(1e-300)
+    lens = torch.ceil(-torch.log(u) * (mean - 0.5)).to(torch.int64)
+    ends = torch.cumsum(lens, 0)
+    ends = ends[ends < n]
+    z = torch.zeros(1, dtype=torch.int64, device=device)
+    return torch.cat([z, ends, torch.full((1,), n, dtype=torch.int64, device=device)])
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -479,6 +494,28 @@ def run_extras(args, x, dev, world, rank, barrier, max_over_ranks, peak):
                      "scan_frac": round(4 * n / ms2 / 1e6 / peak, 4)})
     out["non_pow2_segments"] = {"workload": "segmented reduce / inclusive scan, 2^30 fp16, "
                                             "fp16 out, ragged last segment", "rows": rows}
+    del y
+    # irregular (CSR-offset) segments: geometric lengths
+    rows = []
+    y = torch.empty(n, dtype=torch.float32, device=dev)
+    for mean in (64, 1024, 16384):
+        off = irregular_offsets(n, mean, dev, seed=11 + rank)
+        nseg = off.numel() - 1
+        o = torch.empty(nseg, dtype=torch.float32, device=dev)
+        ms = _time_op(lambda: D.irreg_reduce(x, off, torch.float32, out=o, validate=False), reps,
+                      2, stream, barrier, max_over_ranks)
+        b = 2 * n + 8 * (nseg + 1) + 4 * nseg
+        ms2 = _time_op(lambda: D.irreg_scan(x, off, torch.float32, out=y, validate=False), reps,
+                       2, stream, barrier, max_over_ranks)
+        b2 = 2 * n + 8 * (nseg + 1) + 4 * n
+        rows.append({"mean_seg": mean, "nseg": nseg, "reduce_ms": round(ms, 4),
+                     "reduce_frac": round(b / ms / 1e6 / peak, 4), "scan_ms": round(ms2, 4),
+                     "scan_frac": round(b2 / ms2 / 1e6 / peak, 4)})
+        del off, o
+    out["irregular_segments"] = {
+        "workload": "irregular segmented reduce / inclusive scan, 2^30 fp16, int64 CSR offsets, "
+                    "geometric segment lengths, fp32 out",
+        "bytes": "2n + 8(nseg+1) + 4 nseg (reduce), 2n + 8(nseg+1) + 4n (scan)", "rows": rows}
     del y
     # full ops over 2^33 elements sharded across the ranks
     nf = 1 << FULL_LOG2N
