@@ -517,6 +517,18 @@ def run_extras(args, x, dev, world, rank, barrier, max_over_ranks, peak):
                     "geometric segment lengths, fp32 out",
         "bytes": "2n + 8(nseg+1) + 4 nseg (reduce), 2n + 8(nseg+1) + 4n (scan)", "rows": rows}
     del y
+    # batch-norm statistics consumer, ResNet-50 conv2_x activation shape
+    xbn = gen_device(256 * 256 * 56 * 56, dev, seed=21 + rank).view(256, 256, 56, 56)
+    ms = _time_op(lambda: D.bn_stats(xbn), reps, 2, stream, barrier, max_over_ranks)
+    nb = xbn.numel()
+    out["batch_norm_stats"] = {
+        "workload": "per-channel mean + biased variance, NCHW fp16 (256, 256, 56, 56), fp32 out",
+        "ms": round(ms, 4), "gelem_s": round(nb / ms / 1e6, 1),
+        "gbs_algorithmic": round(2 * nb / ms / 1e6, 1),
+        "frac_algorithmic": round(2 * nb / ms / 1e6 / peak, 4),
+        "gbs_actual": round(4 * nb / ms / 1e6, 1),
+        "passes": "tensor-core segmented reduce (mean) + centred second moment (2 reads of x)"}
+    del xbn
     # full ops over 2^33 elements sharded across the ranks
     nf = 1 << FULL_LOG2N
     lo, hi = PD.even_bounds(nf, world, rank)

@@ -70,6 +70,7 @@ extern "C" {
 /* op ids for tc_workspace_bytes */
 #define TC_OP_REDUCE 0
 #define TC_OP_SCAN 1
+#define TC_OP_BN_STATS 2       /* tc_workspace_bytes(TC_OP_BN_STATS, N*C*HW, HW) */
 
 /* Bytes of device workspace an op over n elements with segment size seg
  * needs (seg >= n means one segment: the grid/full variants). */
@@ -140,6 +141,17 @@ int tc_irreg_scan(const void* x, int in_dtype, int64_t n, const int64_t* offsets
                   void* out, int out_dtype, int exclusive, void* ws, size_t ws_bytes,
                   void* stream);
 
+/* Batch-norm statistics (the TCU-reduction consumer the paper sketches,
+ * PAPER.md:2185-2217) of an NCHW-contiguous tensor
+ * x[N][C][HW] (in_dtype TC_F16 | TC_BF16): per channel c, mean[c] and the
+ * biased variance var[c] over the N*HW elements, out_dtype TC_F32 | TC_F64
+ * (DEVICE arrays of C).  Pass 1 = tc_seg_reduce_ex with seg = HW on the
+ * tensor core (the mean, as in the paper); pass 2 = the centred second
+ * moment on CUDA cores; pass 3 combines.  ws >= tc_workspace_bytes(
+ * TC_OP_BN_STATS, N*C*HW, HW).  Three launches, stream-ordered. */
+int tc_bn_stats(const void* x, int in_dtype, int64_t N, int64_t C, int64_t HW, void* mean,
+                void* var, int out_dtype, void* ws, size_t ws_bytes, void* stream);
+
 /* Human-readable name of a status code. */
 const char* tc_status_string(int status);
 
@@ -152,7 +164,7 @@ uint64_t tc_launch_count(void);
 void tc_reset_launch_count(void);
 
 /* ABI version: (major << 16) | minor.  1.1 added the *_ex entry points,
- * 1.2 the tc_irreg_* entry points. */
+ * 1.2 the tc_irreg_* entry points, 1.3 tc_bn_stats. */
 int tc_abi_version(void);
 
 #ifdef __cplusplus

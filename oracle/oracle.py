@@ -221,6 +221,20 @@ def ref_irreg_scan(values, offsets, inclusive=True):
     return ex.astype(np.float64)
 
 
+# ------------------------------------------------ batch-norm statistics
+# Extension: the paper's TCU-reduction consumer
+# (mu_B = mean of the mini-batch per channel, sigma_B^2 =
+# mean of (x - mu_B)^2), restated in binary64 for an (N, C, *spatial) array.
+
+
+def ref_bn_stats(x):
+    a = np.asarray(x).astype(np.float64)
+    a = a.reshape(a.shape[0], a.shape[1], -1)
+    mean = a.mean(axis=(0, 2))
+    var = ((a - mean[None, :, None]) ** 2).mean(axis=(0, 2))
+    return mean, var
+
+
 # ------------------------------------------------ tile-engine arithmetic (sim)
 
 

@@ -187,3 +187,29 @@ def irreg_scan(x: torch.Tensor, offsets: torch.Tensor, out_dtype=torch.float16, 
                                   out.data_ptr(), _DT[out.dtype], 1 if exclusive else 0,
                                   ws.data_ptr(), ws.numel(), _stream_ptr(x.device)))
     return out
+
+
+def bn_stats(x: torch.Tensor, out_dtype=torch.float32):
+    """Per-channel (mean, biased variance) of an NCHW-contiguous CUDA tensor
+    x of shape (N, C, *spatial), fp16 or bf16 (tc_bn_stats)."""
+    if not x.is_cuda:
+        raise ValueError("device entry points take CUDA tensors")
+    if x.dim() < 2:
+        raise BadLengthError("batch-norm statistics need an (N, C, ...) tensor")
+    N, C = int(x.shape[0]), int(x.shape[1])
+    HW = 1
+    for d in x.shape[2:]:
+        HW *= int(d)
+    if N * C * HW == 0:
+        raise BadLengthError("batch-norm statistics of an empty tensor")
+    if x.dtype not in _IN:
+        x = x.to(torch.float16)
+    if not x.is_contiguous() or x.data_ptr() % 16:
+        x = x.contiguous().clone()
+    mean = torch.empty(C, dtype=out_dtype, device=x.device)
+    var = torch.empty(C, dtype=out_dtype, device=x.device)
+    ws = workspace(_lib.TC_OP_BN_STATS, N * C * HW, HW, x.device)
+    _check(_lib.lib.tc_bn_stats(x.data_ptr(), _IN[x.dtype], N, C, HW, mean.data_ptr(),
+                                var.data_ptr(), _DT[out_dtype], ws.data_ptr(), ws.numel(),
+                                _stream_ptr(x.device)))
+    return mean, var

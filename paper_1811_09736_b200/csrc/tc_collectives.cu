@@ -633,6 +633,84 @@ __global__ void __launch_bounds__(kTailThreads) irreg_tail_kernel(const __half* 
   }
 }
 
+// ------------------------------------------------------------------------
+// Batch-norm statistics (the paper's TCU-reduction consumer, PAPER.md:
+// 2185-2217).  x is NCHW-contiguous: the HW
+// elements of (n, c) are one segment.  Pass 1 is the tensor-core segmented
+// reduce (s = HW, fp64 sums) -- the mean, which is what the paper puts on
+// the TCU.  Pass 2 (CUDA cores, like the paper's "all other operations")
+// accumulates the CENTRED second moment sum (x - K)^2 with K = fp32(mean),
+// split over n, and pass 3 combines the splits in order:
+// var = S / M - (mean - K)^2 (the shifted-data formula: exact in real
+// arithmetic, no E[x^2] - mean^2 cancellation).
+constexpr int kBnThreads = 256;
+
+__device__ __forceinline__ double block_sum_d(double v, double* sred) {
+  v = warp_sum_d(v);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += sred[w];
+  __syncthreads();
+  return t;
+}
+
+// mean of channel c from pass 1's (n, c) sums, fixed order
+__device__ __forceinline__ double bn_channel_mean(const double* segsum, long long N, long long C,
+                                                  long long HW, long long c, double* sred) {
+  double m = 0.0;
+  for (long long n = threadIdx.x; n < N; n += blockDim.x) m += segsum[n * C + c];
+  return block_sum_d(m, sred) / static_cast<double>(N * HW);
+}
+
+__global__ void __launch_bounds__(kBnThreads) bn_centred_kernel(const __half* x, int in_bf16,
+                                                                long long N, long long C,
+                                                                long long HW, const double* segsum,
+                                                                double* part) {
+  __shared__ double sred[kBnThreads / 32];
+  const long long c = blockIdx.x;
+  const int splits = gridDim.y, sp = blockIdx.y;
+  const double mean = bn_channel_mean(segsum, N, C, HW, c, sred);
+  const float k = static_cast<float>(mean);
+  const bool bf16 = in_bf16 != 0;
+  const long long n0 = N * sp / splits, n1 = N * (sp + 1) / splits;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kWarps = kBnThreads / 32;
+  double acc = 0.0;
+  // one warp per (n, c) segment, lanes stride the HW contiguous elements
+  for (long long nn = n0 + warp; nn < n1; nn += kWarps) {
+    const long long base = (nn * C + c) * HW;
+    float fs = 0.f;
+    for (long long i = lane; i < HW; i += 32) {
+      const float d = in_to_float(x, base + i, bf16) - k;
+      fs = fmaf(d, d, fs);
+    }
+    acc += static_cast<double>(fs);
+  }
+  const double t = block_sum_d(acc, sred);
+  if (threadIdx.x == 0) part[c * splits + sp] = t;
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(kBnThreads) bn_finish_kernel(long long N, long long C,
+                                                               long long HW, const double* segsum,
+                                                               const double* part, int splits,
+                                                               OutT* mean_out, OutT* var_out) {
+  __shared__ double sred[kBnThreads / 32];
+  const long long c = blockIdx.x;
+  const double mean = bn_channel_mean(segsum, N, C, HW, c, sred);
+  if (threadIdx.x == 0) {
+    double s2 = 0.0;
+    for (int sp = 0; sp < splits; ++sp) s2 += part[c * splits + sp];
+    const double k = static_cast<double>(static_cast<float>(mean));
+    const double m = static_cast<double>(N * HW);
+    double var = s2 / m - (mean - k) * (mean - k);
+    if (var < 0.0) var = 0.0;
+    mean_out[c] = static_cast<OutT>(mean);
+    var_out[c] = static_cast<OutT>(var);
+  }
+}
+
 template <int OP, int GR, int MODE, typename OutT>
 __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, GR, MODE, OutT>::MINB))
     seg_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
@@ -1955,10 +2033,11 @@ static long long gcd_ll(long long a, long long b) {
 static long long chunk_slots(long long n) { return (n + kTileElems - 1) / kTileElems + kMaxCtas; }
 
 static size_t ws_need(int op, long long n, long long seg) {
-  (void)seg;
   size_t b = kWsLookback;
   if (op == TC_OP_SCAN)
     b += static_cast<size_t>(chunk_slots(n)) * sizeof(uint64_t) + 64;
+  if (op == TC_OP_BN_STATS)  // (n, c) segment sums + per-(c, split) centred partials
+    b += 2 * sizeof(double) * static_cast<size_t>((n + seg - 1) / (seg > 0 ? seg : 1)) + 512;
   return (b + 255) & ~size_t(255);
 }
 
@@ -2383,6 +2462,61 @@ int tc_irreg_scan(const void* x, int in_dtype, int64_t n, const int64_t* offsets
   return fn(p, out_dtype == TC_F16 ? 2 : 4, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int tc_bn_stats(const void* x, int in_dtype, int64_t N, int64_t C, int64_t HW, void* mean,
+                void* var, int out_dtype, void* ws, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  if (N < 1 || C < 1 || HW < 1 || N > (1LL << 37) / C / HW) {
+    set_err("batch-norm shape outside 1 <= N*C*HW < 2^37 (N*C = %s%lld)", "", N * C);
+    return TC_BAD_LENGTH;
+  }
+  if (!mean || !var) {
+    set_err("null pointer argument%s%lld", "", 0);
+    return TC_BAD_CONFIG;
+  }
+  if (out_dtype != TC_F32 && out_dtype != TC_F64) {
+    set_err("batch-norm statistics are F32 or F64, got %s%lld", "", out_dtype);
+    return TC_BAD_CONFIG;
+  }
+  const long long n = N * C * HW;
+  if (ws_bytes < ws_need(TC_OP_BN_STATS, n, HW)) {
+    set_err("workspace too small: need %s%lld bytes", "", (long long)ws_need(TC_OP_BN_STATS, n, HW));
+    return TC_WORKSPACE_TOO_SMALL;
+  }
+  // pass 1: (n, c) segment sums on the tensor core, fp64, into the workspace tail
+  char* w = reinterpret_cast<char*>(ws);
+  const size_t base = ws_need(TC_OP_REDUCE, n, HW);
+  double* segsum = reinterpret_cast<double*>(w + base);
+  double* part = segsum + N * C;
+  int rc = tc_seg_reduce_ex(x, in_dtype, n, HW, segsum, TC_F64, ws, base, stream);
+  if (rc) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const DevInfo di = dev_info(dev);
+  long long splits = (2LL * (di.sms > 0 ? di.sms : 148) + C - 1) / C;
+  if (splits > N) splits = N;
+  if (splits > 65535) splits = 65535;
+  if (splits < 1) splits = 1;
+  bn_centred_kernel<<<dim3(static_cast<unsigned>(C), static_cast<unsigned>(splits)), kBnThreads, 0,
+                      st>>>(reinterpret_cast<const __half*>(x), in_dtype == TC_BF16 ? 1 : 0, N, C,
+                            HW, segsum, part);
+  if (out_dtype == TC_F32)
+    bn_finish_kernel<float><<<static_cast<unsigned>(C), kBnThreads, 0, st>>>(
+        N, C, HW, segsum, part, static_cast<int>(splits), reinterpret_cast<float*>(mean),
+        reinterpret_cast<float*>(var));
+  else
+    bn_finish_kernel<double><<<static_cast<unsigned>(C), kBnThreads, 0, st>>>(
+        N, C, HW, segsum, part, static_cast<int>(splits), reinterpret_cast<double*>(mean),
+        reinterpret_cast<double*>(var));
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_err("kernel launch failed: %s%lld", cudaGetErrorString(e), 0);
+    return TC_CUDA_ERROR;
+  }
+  g_launches += 2;
+  return TC_OK;
+}
+
 const char* tc_status_string(int s) {
   switch (s) {
     case TC_OK: return "ok";
@@ -2401,6 +2535,6 @@ const char* tc_last_error(void) { return g_err; }
 uint64_t tc_launch_count(void) { return g_launches; }
 void tc_reset_launch_count(void) { g_launches = 0; }
 
-int tc_abi_version(void) { return (1 << 16) | 2; }
+int tc_abi_version(void) { return (1 << 16) | 3; }
 
 }  // extern "C"

@@ -226,3 +226,20 @@ def test_irregular_no_cpu_fallback():
         ht.irregular_segmented_reduce(np.ones(64, np.float16), [0, 10, 64])
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         ht.irregular_segmented_scan(np.ones(64, np.float16), [0, 10, 64])
+
+
+def test_batchnorm_validation_before_device():
+    with pytest.raises(BadLengthError):
+        ht.batch_norm_stats(np.ones(10, np.float16))
+    with pytest.raises(BadLengthError):
+        ht.batch_norm_stats(np.ones((0, 3), np.float16))
+    L = _lib.lib
+    ws = ctypes.create_string_buffer(1 << 16)
+    wsp = (ctypes.addressof(ws) + 255) & ~255
+    xp, m, v = 1 << 20, 2 << 20, 3 << 20
+    assert L.tc_bn_stats(xp, 0, 0, 3, 4, m, v, _lib.TC_F32, wsp, 60000, None) == _lib.TC_BAD_LENGTH
+    assert L.tc_bn_stats(xp, 0, 2, 3, 4, m, v, _lib.TC_F16, wsp, 60000, None) == _lib.TC_BAD_CONFIG
+    assert L.tc_bn_stats(xp, 0, 2, 3, 4, None, v, _lib.TC_F32, wsp, 60000, None) == _lib.TC_BAD_CONFIG
+    assert L.tc_bn_stats(xp, 0, 2, 3, 4, m, v, _lib.TC_F32, wsp, 10, None) == _lib.TC_WORKSPACE_TOO_SMALL
+    need = L.tc_workspace_bytes(_lib.TC_OP_BN_STATS, 2 * 3 * 4, 4)
+    assert need > L.tc_workspace_bytes(_lib.TC_OP_REDUCE, 2 * 3 * 4, 4)

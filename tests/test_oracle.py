@@ -189,3 +189,14 @@ def test_irregular_oracle_against_direct_loops():
             assert np.allclose(s[a:b], c, rtol=1e-14, atol=0)
             if b > a:
                 assert e[a] == 0 and np.allclose(e[a + 1:b], c[:-1], rtol=1e-14, atol=0)
+
+
+def test_bn_oracle_definition():
+    """ref_bn_stats restates PAPER.md:2195-2203 (mu_B, sigma_B^2 per channel)."""
+    rng = np.random.default_rng(0)
+    x = rng.random((3, 4, 5, 6))
+    m, v = O.ref_bn_stats(x)
+    for c in range(4):
+        vals = x[:, c].reshape(-1)
+        assert m[c] == pytest.approx(vals.mean(), rel=1e-14)
+        assert v[c] == pytest.approx(((vals - vals.mean()) ** 2).mean(), rel=1e-12)
