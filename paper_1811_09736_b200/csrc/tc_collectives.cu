@@ -71,6 +71,7 @@
 #include <string.h>
 
 #include <atomic>
+#include <type_traits>
 #include <mutex>
 
 #include "sm100_ptx.cuh"
@@ -677,16 +678,45 @@ __global__ void __launch_bounds__(kBnThreads) bn_centred_kernel(const __half* x,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kWarps = kBnThreads / 32;
   double acc = 0.0;
-  // one warp per (n, c) segment, lanes stride the HW contiguous elements
-  for (long long nn = n0 + warp; nn < n1; nn += kWarps) {
-    const long long base = (nn * C + c) * HW;
-    float fs = 0.f;
-    for (long long i = lane; i < HW; i += 32) {
-      const float d = in_to_float(x, base + i, bf16) - k;
-      fs = fmaf(d, d, fs);
+  // one warp per (n, c) segment; vector width = the segment alignment
+  // (HW % 8 == 0: 16-B loads, % 4: 8-B, % 2: 4-B, else 2-B), two in flight
+  auto run = [&](auto vec_tag) {
+    constexpr int V = decltype(vec_tag)::value;  // elements per load
+    using VT = typename std::conditional<V == 8, uint4,
+               typename std::conditional<V == 4, uint2,
+               typename std::conditional<V == 2, uint32_t, unsigned short>::type>::type>::type;
+    auto sq = [&](const VT& w, float& fs) {
+      const unsigned short* h = reinterpret_cast<const unsigned short*>(&w);
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        const float f = bf16 ? __uint_as_float(static_cast<uint32_t>(h[q]) << 16)
+                             : __half2float(__ushort_as_half(h[q]));
+        const float a = f - k;
+        fs = fmaf(a, a, fs);
+      }
+    };
+    const long long nv = HW / V;
+    for (long long nn = n0 + warp; nn < n1; nn += kWarps) {
+      const VT* xv = reinterpret_cast<const VT*>(x + (nn * C + c) * HW);
+      float fs = 0.f;
+      long long i = lane;
+      for (; i + 32 < nv; i += 64) {
+        const VT a = xv[i], b = xv[i + 32];
+        sq(a, fs);
+        sq(b, fs);
+      }
+      if (i < nv) sq(xv[i], fs);
+      acc += static_cast<double>(fs);
     }
-    acc += static_cast<double>(fs);
-  }
+  };
+  if ((HW & 7) == 0)
+    run(std::integral_constant<int, 8>{});
+  else if ((HW & 3) == 0)
+    run(std::integral_constant<int, 4>{});
+  else if ((HW & 1) == 0)
+    run(std::integral_constant<int, 2>{});
+  else
+    run(std::integral_constant<int, 1>{});
   const double t = block_sum_d(acc, sred);
   if (threadIdx.x == 0) part[c * splits + sp] = t;
 }
