@@ -47,15 +47,22 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
 // The spin loop lives inside the asm block: to the compiler this is straight-
 // line code, so it cannot split the warp here (a C++ retry loop makes every
 // later warp shuffle compile to the slow WARPSYNC.COLLECTIVE emulation).
+// The suspend-time hint (ns) lets the hardware park the waiting warp until
+// the phase completes instead of re-issuing try_wait: spinning producer /
+// MMA warps otherwise take issue slots from the epilogue warps sharing their
+// SM sub-partitions.
+#ifndef TC_MBAR_SUSPEND_NS
+#define TC_MBAR_SUSPEND_NS 0x989680
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
       "TC_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
       "@!P1 bra TC_WAIT;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "n"(TC_MBAR_SUSPEND_NS)
       : "memory");
 }
 

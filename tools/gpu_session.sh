@@ -29,6 +29,20 @@ for p in $PARTS; do
         ncu -i "$OUT/prof_$1_$2_$3.ncu-rep" --page raw --csv > "$OUT/prof_$1_$2_$3.raw.csv" 2>/dev/null
         [ -n "${KEEP_REP:-}" ] || rm -f "$OUT/prof_$1_$2_$3.ncu-rep"
       done;;
+    prof2)
+      # widened rows: irregular segments (geometric mean 64 / 1024) and batch-norm statistics
+      for cfg in "reduce 64 f32" "reduce 1024 f32" "scan 1024 f32"; do
+        set -- $cfg
+        tag=irreg_$1_$2_$3
+        timeout 600 ncu --set full --clock-control none --import-source on -k regex:seg_kernel -s 2 -c 1 \
+          -o "$OUT/prof_$tag" -f python tools/prof_irreg.py $1 $2 $3 3 > "$OUT/prof_$tag.log" 2>&1; echo "prof $tag rc=$?"
+        python tools/ncu_summary.py "$OUT/prof_$tag.ncu-rep" > "$OUT/prof_$tag.txt" 2>&1
+        rm -f "$OUT/prof_$tag.ncu-rep"
+      done
+      timeout 600 ncu --set full --clock-control none -k regex:"seg_kernel|bn_" -s 3 -c 3 \
+        -o "$OUT/prof_bn" -f python tools/prof_bn.py 256 256 56 56 3 > "$OUT/prof_bn.log" 2>&1; echo "prof bn rc=$?"
+      python tools/ncu_summary.py "$OUT/prof_bn.ncu-rep" > "$OUT/prof_bn.txt" 2>&1
+      rm -f "$OUT/prof_bn.ncu-rep";;
     probe)
       timeout 600 python tests/perf_probe.py > "$OUT/perf_probe.log" 2>&1; echo "probe rc=$?"; cat "$OUT/perf_probe.log";;
   esac
