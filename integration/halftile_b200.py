@@ -55,6 +55,8 @@ def _load():
     tc.tc_seg_reduce.argtypes = [vp, i64, i64, vp, ci, vp, sz, vp]
     tc.tc_seg_scan.restype = ci
     tc.tc_seg_scan.argtypes = [vp, i64, i64, vp, ci, ci, vp, vp, vp, sz, vp]
+    tc.tc_irreg_reduce.restype = ci
+    tc.tc_irreg_reduce.argtypes = [vp, ci, i64, vp, i64, vp, ci, vp, sz, vp]
     tc.tc_last_error.restype = ctypes.c_char_p
     name = ctypes.util.find_library("cudart") or "libcudart.so"
     try:
@@ -151,3 +153,25 @@ def seg_reduce(values, seg_size, acc_dtype=np.float16):
 def seg_scan(values, seg_size, acc_dtype=np.float16, inclusive=True):
     """n segmented prefix sums (halftile.segmented_scan semantics)."""
     return _run(values, seg_size, acc_dtype, TC_OP_SCAN, inclusive)
+
+
+def irregular_reduce(values, offsets, acc_dtype=np.float32):
+    """Sums of values[offsets[k]:offsets[k+1]] (tc_irreg_reduce; extension)."""
+    if not available():
+        raise B200Error("no CUDA device / library")
+    x = np.ascontiguousarray(values, dtype=np.float16)
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    n, nseg = x.size, off.size - 1
+    if nseg < 1 or off[0] != 0 or off[-1] != n or np.any(np.diff(off) < 0):
+        raise B200Error("offsets must be non-decreasing from 0 to len(values)")
+    out_dt = np.dtype(acc_dtype)
+    out = np.empty(nseg, dtype=out_dt)
+    code = TC_F32 if out_dt == np.float32 else TC_F16
+    wsb = _tc.tc_workspace_bytes(TC_OP_REDUCE, n, n)
+    with _Dev(x.nbytes) as dx, _Dev(off.nbytes) as dof, _Dev(out.nbytes) as do, _Dev(wsb) as dw:
+        _cuda(_rt.cudaMemset(dw.p, 0, wsb))
+        _cuda(_rt.cudaMemcpy(dx.p, x.ctypes.data, x.nbytes, _H2D))
+        _cuda(_rt.cudaMemcpy(dof.p, off.ctypes.data, off.nbytes, _H2D))
+        _check(_tc.tc_irreg_reduce(dx.p, TC_F16, n, dof.p, nseg, do.p, code, dw.p, wsb, None))
+        _cuda(_rt.cudaMemcpy(out.ctypes.data, do.p, out.nbytes, _D2H))
+    return out

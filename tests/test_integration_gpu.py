@@ -24,3 +24,14 @@ def test_binding_reduce_and_scan_exact(s, cuda):
     assert np.array_equal(scans, O.ref_seg_scan(x, s).astype(np.float32))
     ex = B.seg_scan(x, s, np.float32, inclusive=False)
     assert np.array_equal(ex, O.ref_seg_scan(x, s, inclusive=False).astype(np.float32))
+
+
+def test_binding_irregular_reduce(cuda):
+    from integration import halftile_b200 as B
+
+    rng = np.random.default_rng(5)
+    n = (1 << 20) + 77
+    x = rng.integers(0, 4, n).astype(np.float16)
+    off = O.random_offsets(rng, n, 100, empty_frac=0.2)
+    got = B.irregular_reduce(x, off, np.float32)
+    assert np.array_equal(got, O.ref_irreg_reduce(x, off).astype(np.float32))
