@@ -189,8 +189,13 @@ struct Cfg {
   static constexpr int MINB = (CHUNK || (OP == OP_SCAN && GR >= 32)) ? 1
                               : (OP == OP_REDUCE && MODE == MODE_GENERAL && GR >= 8 && GR <= 32) ? 3
                                                                                        : 2;
+  // fp32-output scans at 2 CTAs/SM fit either 4 input stages + 1 output
+  // buffer or 2 + 2.  The pair-scan modes (GENERAL, IRREG) prefer 2 + 2
+  // (measured: s = 300 79 -> 87 % of copy bandwidth), the others 4 + 1.
+  static constexpr bool SCAN32_2BUF = (MODE == MODE_GENERAL || MODE == MODE_IRREG);
   static constexpr int STAGES = CHUNK ? 8
                                 : (OP == OP_REDUCE) ? (MINB == 3 ? 4 : MINB == 2 ? 6 : 8)
+                                : (MINB == 2 && sizeof(OutT) == 4 && SCAN32_2BUF) ? 2
                                                     : (MINB == 2 ? 4 : 6);
   static constexpr int ACC = CHUNK ? 8 : 4;  // TMEM accumulator stages (tiles)
   // CHUNK with one granule per row splits the epilogue: warps 2..5 write the
@@ -203,7 +208,8 @@ struct Cfg {
   // output + 4 aggregate warps
   static constexpr int TEMPTY = AGG ? 8 : kEpiThreads;
   static constexpr int TMEM_COLS = pow2_at_least(ACC * N);
-  static constexpr int OUT_BUFS = (OP == OP_SCAN) ? ((sizeof(OutT) == 4 && MINB == 2) ? 1 : 2) : 0;
+  static constexpr int OUT_BUFS =
+      (OP == OP_SCAN) ? ((sizeof(OutT) == 4 && MINB == 2 && !SCAN32_2BUF) ? 1 : 2) : 0;
   static constexpr uint32_t OUT_BYTES = kTileElems * sizeof(OutT);
   static constexpr uint32_t OFF_B = STAGES * kTileBytes;
   static constexpr uint32_t OFF_OUT = OFF_B + ((N * 128 + 1023) / 1024) * 1024;
