@@ -2109,8 +2109,12 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
   constexpr uint32_t smem = smem_bytes<OP, GR, MODE, OutT>();
   static_assert(smem <= 232448, "shared memory budget");
   auto kern = seg_kernel<OP, GR, MODE, OutT>;
-  static std::atomic<int> attr_done{0};
-  if (!attr_done.load()) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  // function attributes are per device: set them once on each device used
+  static std::atomic<uint64_t> attr_done{0};
+  const uint64_t dev_bit = 1ull << (dev & 63);
+  if (!(attr_done.load() & dev_bit)) {
     // max shared-memory carveout, so MINB = 2 kernels really get 2 CTAs/SM
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
@@ -2119,10 +2123,8 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
       set_err("cudaFuncSetAttribute failed: %s%lld", cudaGetErrorString(cudaGetLastError()), 0);
       return TC_CUDA_ERROR;
     }
-    attr_done.store(1);
+    attr_done.fetch_or(dev_bit);
   }
-  int dev = 0;
-  cudaGetDevice(&dev);
   DevInfo di = dev_info(dev);
   if (!di.ok || di.major < 10) {
     set_err("no sm_100 device (compute capability major %s%lld)", "", di.major);
