@@ -138,6 +138,7 @@ struct Params {
   int exclusive;
   int need_fixup;  // reduce: segments may straddle CTA ranges
   const long long* offs;  // IRREG: nseg + 1 non-decreasing offsets, offs[0] = 0, offs[nseg] = n
+  int cum_b;              // GENERAL reduce with m >= GR: cumulative (granule-prefix) B matrix
 };
 
 template <typename T>
@@ -258,7 +259,7 @@ constexpr uint32_t smem_bytes() {
 // Constant B operand, K-major, 128-B swizzled: row n (N index) holds B[k][n]
 // for k = 0..63.  Reduce: granule indicator.  Scan: block-diag upper-tri U.
 template <int OP, int GR, int N>
-__device__ void build_b(uint8_t* sb, uint16_t one_bits) {
+__device__ void build_b(uint8_t* sb, uint16_t one_bits, bool cum = false) {
   constexpr int G = 64 / GR;
   for (int idx = threadIdx.x; idx < N * 8; idx += blockDim.x) {
     const int n = idx >> 3, pos = idx & 7;
@@ -269,7 +270,7 @@ __device__ void build_b(uint8_t* sb, uint16_t one_bits) {
       const int k = lc * 8 + e;
       bool one;
       if (OP == OP_REDUCE)
-        one = (n < GR) && (k / G == n);
+        one = (n < GR) && (cum ? (k / G <= n) : (k / G == n));
       else
         one = (k / G == n / G) && (k <= n);
       h[e] = one ? one_bits : 0;
@@ -840,7 +841,8 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
     ptx::tmem_alloc(&misc->tmem_base, C::TMEM_COLS);
     ptx::tmem_relinquish();
   }
-  build_b<(C::IRREG ? OP_SCAN : OP), GR, N>(smem + C::OFF_B, p.in_bf16 ? 0x3F80 : 0x3C00);
+  build_b<(C::IRREG ? OP_SCAN : OP), GR, N>(smem + C::OFF_B, p.in_bf16 ? 0x3F80 : 0x3C00,
+                                            p.cum_b != 0);
   if constexpr (C::IRREG) {
     for (int k = threadIdx.x; k < 2 * kTileRows; k += blockDim.x) (&misc->icnt[0][0])[k] = 0;
   }
@@ -1434,25 +1436,43 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
             const long long rem0 = p.m - 1 - qmod;
             const long long dl = p.qlast - q0;
             const int lastj = dl < GR ? static_cast<int>(dl) : GR;
-            const int m32 = p.m < (1LL << 20) ? static_cast<int>(p.m) : (1 << 20);
-            int e = rem0 < GR ? static_cast<int>(rem0) : GR;
             long long sg = qdiv;        // segment containing granule q0 + j
             const long long seg0 = sg;  // segment closed by the row's first end
             float run = 0.f, head = 0.f;
             int seen = 0;
+            if (p.cum_b && dl >= GR && row != p.rows_full) {
+              // segments of >= one row (m >= GR) with the cumulative B: the
+              // columns are granule PREFIXES, at most one segment ends in the
+              // row (granule e0) -> head = P[e0], tail = P[GR-1] - P[e0]
+              const int e0 = rem0 < GR ? static_cast<int>(rem0) : -1;
+              float hv = gs[0];
   #pragma unroll
-            for (int j = 0; j < GR; ++j) {
-              run += gs[j];
-              if ((j == e && j <= lastj) || j == lastj) {
-                if (!seen) {
-                  head = run;  // needs the carry from earlier rows / tiles
-                  seen = 1;
-                } else {
-                  out[sg] = cvt_out<OutT>(run);  // segment wholly inside this row
+              for (int j = 1; j < GR; ++j) hv = (j == e0) ? gs[j] : hv;
+              seen = e0 >= 0;
+              head = seen ? hv : 0.f;
+              run = seen ? gs[GR - 1] - hv : gs[GR - 1];
+            } else {
+              if (p.cum_b && row != p.rows_full) {
+                // the row holding the input's last granule (or padding): back to sums
+  #pragma unroll
+                for (int j = GR - 1; j > 0; --j) gs[j] -= gs[j - 1];
+              }
+              const int m32 = p.m < (1LL << 20) ? static_cast<int>(p.m) : (1 << 20);
+              int e = rem0 < GR ? static_cast<int>(rem0) : GR;
+  #pragma unroll
+              for (int j = 0; j < GR; ++j) {
+                run += gs[j];
+                if ((j == e && j <= lastj) || j == lastj) {
+                  if (!seen) {
+                    head = run;  // needs the carry from earlier rows / tiles
+                    seen = 1;
+                  } else {
+                    out[sg] = cvt_out<OutT>(run);  // segment wholly inside this row
+                  }
+                  ++sg;
+                  run = 0.f;
+                  e += m32;
                 }
-                ++sg;
-                run = 0.f;
-                e += m32;
               }
             }
             float v = run;
@@ -2341,6 +2361,9 @@ static Params make_params(const void* x, long long n, long long seg, void* out, 
   size_t off = kWsLookback;
   p.u_word = reinterpret_cast<uint64_t*>(w + off);
   p.ck = 1;
+  // GENERAL reduce whose segments span at least a row: B = granule prefixes
+  // (B[k][j] = [k/g <= j]) so one select finds the row's single segment end
+  p.cum_b = (op == TC_OP_REDUCE && mode == MODE_GENERAL && p.m >= gr && gr > 1) ? 1 : 0;
   p.need_fixup = (op == TC_OP_REDUCE && (mode == MODE_TILES || mode == MODE_GENERAL) &&
                   (kTileElems % seg != 0))
                      ? 1
@@ -2472,6 +2495,7 @@ static Params irreg_params(const void* x, int in_dtype, int64_t n, const int64_t
   p.in_bf16 = (in_dtype == TC_BF16) ? 1 : 0;
   p.offs = reinterpret_cast<const long long*>(offsets);
   p.nseg = nseg;
+  p.cum_b = 0;
   p.need_fixup = (op == TC_OP_REDUCE) ? 1 : 0;
   return p;
 }
