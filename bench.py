@@ -262,10 +262,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_DIST_BACKEND=gloo (test only): several ranks may share one GPU,
+    # which NCCL refuses -- used to exercise the N > 1 path on a 1-GPU box
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     import paper_1811_09736_b200 as ht
     from paper_1811_09736_b200 import _device as D
@@ -273,7 +280,10 @@ def run_ours(args):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
         torch.cuda.synchronize()
 
     def max_over_ranks(v):
@@ -443,6 +453,12 @@ def _time_op(fn, reps, warm, stream, barrier, max_over_ranks):
     return max_over_ranks(a.elapsed_time(b)) / reps
 
 
+def dist_backend():
+    import torch.distributed as dist
+
+    return str(dist.get_backend()).upper() if dist.is_initialized() else "none"
+
+
 def run_extras(args, x, dev, world, rank, barrier, max_over_ranks, peak):
     """configs[2..4]: scan sweep (1 GPU each rank), full reduce / full
     exclusive scan of 2^33 elements sharded over the ranks."""
@@ -543,8 +559,8 @@ def run_extras(args, x, dev, world, rank, barrier, max_over_ranks, peak):
     out["full_reduce_2^33"] = {"ms": round(ms, 4), "gelem_s": round(nf / ms / 1e6, 1),
                                "gbs_per_gpu": round(b / ms / 1e6, 1),
                                "frac": round(b / ms / 1e6 / peak, 4),
-                               "exchange": "NCCL all_gather of fp64 partials" if world > 1
-                               else "none"}
+                               "exchange": (f"{dist_backend()} all_gather of fp64 partials"
+                                            if world > 1 else "none")}
     yl = torch.empty(hi - lo, dtype=torch.float32, device=dev)
 
     def fscan():
