@@ -2172,7 +2172,7 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
     // (a GENERAL reduce on the cumulative-B path is light enough for 2)
     per_sm = (MODE == MODE_GENERAL && OP == OP_REDUCE && p0.cum_b) ? 2
              : (MODE == MODE_GENERAL || MODE == MODE_IRREG) ? Cfg<OP, GR, MODE, OutT>::MINB
-             : ((OP == OP_REDUCE && MODE == MODE_ROWS && p0.log2m >= 4) ||
+             : ((OP == OP_REDUCE && MODE == MODE_ROWS && p0.log2m >= 4 && p0.log2m < 7) ||
                 (OP == OP_SCAN && MODE == MODE_LOCAL && sizeof(OutT) == 4))
                  ? 2
                  : 1;
