@@ -94,6 +94,8 @@ constexpr int MODE_TILES = 2;
 constexpr int MODE_GENERAL = 3;
 constexpr int MODE_CHUNK = 4;
 constexpr int MODE_IRREG = 5;  // irregular segments from a CSR offsets array
+constexpr int MODE_GSCR = 6;   // GENERAL reduce, one-element granules, segments < a row:
+                               // the row's granule prefixes staged in SMEM for the ends
 constexpr int kMaxCtas = 1024;                    // persistent grid cap
 constexpr long long kScanPrepassMax = 1LL << 18;  // largest seg whose range-entry carry is recomputed
 constexpr unsigned kFull = 0xffffffffu;
@@ -195,7 +197,9 @@ struct Cfg {
   // (measured: s = 300 79 -> 87 % of copy bandwidth), the others 4 + 1.
   static constexpr bool SCAN32_2BUF = (MODE == MODE_GENERAL || MODE == MODE_IRREG);
   static constexpr int STAGES = CHUNK ? 8
-                                : (OP == OP_REDUCE) ? (MINB == 3 ? 4 : MINB == 2 ? 6 : 8)
+                                : (OP == OP_REDUCE)
+                                    ? ((MINB == 3 || MODE == MODE_GSCR) ? 4
+                                       : MINB == 2 ? 6 : 8)
                                 : (MINB == 2 && sizeof(OutT) == 4 && SCAN32_2BUF) ? 2
                                                     : (MINB == 2 ? 4 : 6);
   static constexpr int ACC = CHUNK ? 8 : 4;  // TMEM accumulator stages (tiles)
@@ -214,7 +218,13 @@ struct Cfg {
   static constexpr uint32_t OUT_BYTES = kTileElems * sizeof(OutT);
   static constexpr uint32_t OFF_B = STAGES * kTileBytes;
   static constexpr uint32_t OFF_OUT = OFF_B + ((N * 128 + 1023) / 1024) * 1024;
-  static constexpr uint32_t OFF_MISC = OFF_OUT + OUT_BUFS * OUT_BYTES;
+  // GENERAL reduce with one-element granules (odd s): each thread's row of
+  // granule prefixes staged in SMEM (row stride 68 floats: conflict-free
+  // 16-B stores) so the row's many segment ends are one load each
+  static constexpr bool SCR = (OP == OP_REDUCE && MODE == MODE_GSCR);
+  static constexpr uint32_t SCR_BYTES = SCR ? kTileRows * 68 * 4 : 0;
+  static constexpr uint32_t OFF_SCR = OFF_OUT + OUT_BUFS * OUT_BYTES;
+  static constexpr uint32_t OFF_MISC = OFF_SCR + SCR_BYTES;
   static constexpr int LD_COLS = (OP == OP_SCAN || IRREG) ? 64 : GR;  // TMEM columns read per tile
   static constexpr bool CONTIG = (MODE != MODE_CHUNK);       // contiguous CTA tile ranges
 };
@@ -905,7 +915,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
     long long q0 = (t_begin * kTileRows + rit) * GR;     // first granule of this row
     long long qmod = 0, qdiv = 0;                        // GENERAL: q0 % m, q0 / m
     long long tpos = 0, tseg = 0;                        // TILES: t % k, t / k
-    if constexpr (MODE == MODE_GENERAL) {
+    if constexpr (MODE == MODE_GENERAL || MODE == MODE_GSCR) {
       qmod = q0 % p.m;
       qdiv = q0 / p.m;
     }
@@ -1440,17 +1450,56 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
             const long long seg0 = sg;  // segment closed by the row's first end
             float run = 0.f, head = 0.f;
             int seen = 0;
-            if (p.cum_b && dl >= GR && row != p.rows_full) {
-              // segments of >= one row (m >= GR) with the cumulative B: the
-              // columns are granule PREFIXES, at most one segment ends in the
-              // row (granule e0) -> head = P[e0], tail = P[GR-1] - P[e0]
+            bool done = false;
+            if constexpr (C::SCR) {
+              if (p.cum_b && dl >= GR && row != p.rows_full && p.m < GR) {
+                // one-element granules, segments shorter than a row: ends at
+                // e0, e0 + m, ... (e0 < m always exists); pieces are
+                // differences of prefixes read back from this row's SMEM copy
+                float* scr = reinterpret_cast<float*>(smem + C::OFF_SCR) + rit * 68;
+  #pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  *reinterpret_cast<float4*>(scr + 4 * j) =
+                      make_float4(gs[4 * j], gs[4 * j + 1], gs[4 * j + 2], gs[4 * j + 3]);
+                const int m32 = static_cast<int>(p.m);
+                int e = static_cast<int>(rem0);
+                float prev = scr[e];  // own row: program order, no barrier
+                head = prev;
+                seen = 1;
+                long long sgi = seg0 + 1;
+                for (e += m32; e < GR; e += m32) {
+                  const float pe = scr[e];
+                  out[sgi++] = cvt_out<OutT>(pe - prev);
+                  prev = pe;
+                }
+                run = gs[GR - 1] - prev;
+                done = true;
+              }
+            }
+            if (done) {
+            } else if (p.cum_b && dl >= GR && row != p.rows_full) {
+              // segments of >= half a row (2m >= GR) with the cumulative B:
+              // the columns are granule PREFIXES and at most two segments end
+              // in the row (granules e0 < e1) -> head = P[e0], the segment
+              // between them = P[e1] - P[e0], tail = P[GR-1] - P[last end]
               const int e0 = rem0 < GR ? static_cast<int>(rem0) : -1;
               float hv = gs[0];
   #pragma unroll
               for (int j = 1; j < GR; ++j) hv = (j == e0) ? gs[j] : hv;
+              float last = hv;
+              if (p.m < GR) {  // uniform: a second end is possible
+                const int e1 = (e0 >= 0 && e0 + p.m < GR) ? e0 + static_cast<int>(p.m) : -1;
+                float hv1 = gs[0];
+  #pragma unroll
+                for (int j = 1; j < GR; ++j) hv1 = (j == e1) ? gs[j] : hv1;
+                if (e1 >= 0) {
+                  out[seg0 + 1] = cvt_out<OutT>(hv1 - hv);  // wholly inside this row
+                  last = hv1;
+                }
+              }
               seen = e0 >= 0;
               head = seen ? hv : 0.f;
-              run = seen ? gs[GR - 1] - hv : gs[GR - 1];
+              run = seen ? gs[GR - 1] - last : gs[GR - 1];
             } else {
               if (p.cum_b && row != p.rows_full) {
                 // the row holding the input's last granule (or padding): back to sums
@@ -2170,7 +2219,7 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
   // match the API.
   if (MODE != MODE_CHUNK) {
     // (a GENERAL reduce on the cumulative-B path is light enough for 2)
-    per_sm = (MODE == MODE_GENERAL && OP == OP_REDUCE && p0.cum_b) ? 2
+    per_sm = ((MODE == MODE_GENERAL && OP == OP_REDUCE && p0.cum_b) || MODE == MODE_GSCR) ? 2
              : (MODE == MODE_GENERAL || MODE == MODE_IRREG) ? Cfg<OP, GR, MODE, OutT>::MINB
              : ((OP == OP_REDUCE && MODE == MODE_ROWS && p0.log2m >= 4 && p0.log2m < 7) ||
                 (OP == OP_SCAN && MODE == MODE_LOCAL && sizeof(OutT) == 4))
@@ -2282,6 +2331,9 @@ static LaunchFn pick(int gr, int mode) {
       if constexpr (OP == OP_SCAN) return pick_gr<OP, MODE_CHUNK, OutT>(gr);
       return nullptr;
     case MODE_IRREG: return gr == 1 ? &launch<OP, 1, MODE_IRREG, OutT> : nullptr;
+    case MODE_GSCR:
+      if constexpr (OP == OP_REDUCE) return gr == 64 ? &launch<OP, 64, MODE_GSCR, OutT> : nullptr;
+      return nullptr;
   }
   return nullptr;
 }
@@ -2363,10 +2415,21 @@ static Params make_params(const void* x, long long n, long long seg, void* out, 
   size_t off = kWsLookback;
   p.u_word = reinterpret_cast<uint64_t*>(w + off);
   p.ck = 1;
-  // GENERAL reduce whose segments span at least a row: B = granule prefixes
-  // (B[k][j] = [k/g <= j]) so one select finds the row's single segment end
-  p.cum_b = (op == TC_OP_REDUCE && mode == MODE_GENERAL && p.m >= gr && gr > 1) ? 1 : 0;
-  p.need_fixup = (op == TC_OP_REDUCE && (mode == MODE_TILES || mode == MODE_GENERAL) &&
+  // GENERAL reduce whose segments span at least a row (or half a row, with
+  // >= 16 granules per row): B = granule prefixes (B[k][j] = [k/g <= j]) so
+  // one or two selects find the row's segment ends (measured: at 4-8
+  // granules per row the granule walk is as fast)
+  p.cum_b = (op == TC_OP_REDUCE && mode == MODE_GENERAL && gr > 1 &&
+             (p.m >= gr || (2 * p.m >= gr && gr >= 16) || gr == 64))
+                ? 1
+                : 0;
+  // one-element granules and segments shorter than a row: many ends per row,
+  // looked up from an SMEM copy of the row's prefixes (its own mode, so the
+  // longer-segment GENERAL kernels keep their 6-stage ring)
+  if (op == TC_OP_REDUCE && mode == MODE_GENERAL && gr == 64 && p.m < gr) mode = MODE_GSCR;
+  *mode_out = mode;
+  p.need_fixup = (op == TC_OP_REDUCE &&
+                  (mode == MODE_TILES || mode == MODE_GENERAL || mode == MODE_GSCR) &&
                   (kTileElems % seg != 0))
                      ? 1
                      : 0;
