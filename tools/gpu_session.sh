@@ -20,7 +20,7 @@ for p in $PARTS; do
       timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
         --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 1 > "$OUT/launches_bench.log" 2>&1; echo "launches rc=$?";;
     prof)
-      CFGS=("reduce 16 f16" "reduce 2048 f16" "reduce 65536 f16" "scan 256 f16" "scan 16384 f32" "scan 1073741824 f32" "scan 300 f16")
+      CFGS=("reduce 16 f16" "reduce 2048 f16" "reduce 65536 f16" "reduce 300 f16" "reduce 17 f16" "scan 256 f16" "scan 16384 f32" "scan 1073741824 f32" "scan 300 f16")
       for cfg in "${CFGS[@]}"; do
         set -- $cfg
         timeout 600 ncu --set full --clock-control none --import-source on -k regex:seg_kernel -s 2 -c 1 \
