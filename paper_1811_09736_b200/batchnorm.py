@@ -58,6 +58,8 @@ def batch_norm(x, weight=None, bias=None, eps: float = 1e-5):
     above; returns (y, mean, var)."""
     import torch
 
+    if not (isinstance(x, torch.Tensor) and x.is_cuda):
+        raise TypeError("batch_norm takes a CUDA tensor (use batch_norm_stats for host arrays)")
     mean, var = batch_norm_stats(x)
     shape = (1, -1) + (1,) * (x.dim() - 2)
     inv = torch.rsqrt(var + eps)
