@@ -397,3 +397,19 @@ def test_nccl_single_rank_sharded_ops(cuda):
         assert np.array_equal(sc.cpu().numpy(), O.ref_seg_scan(x, x.size, inclusive=False).astype(np.float32))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("s", [17, 49, 63, 300, 1001, 100001])
+def test_general_and_odd_segments_2p28(s, cuda):
+    """Large-n parity of the GENERAL-mode paths (cumulative-B one/two-end
+    selects, MODE_GSCR's SMEM-staged ends, the granule walk) against the
+    exact oracle, exact-integer data: fp32 bit-exact, fp16 = fp16(exact)."""
+    rng = np.random.default_rng(s)
+    n = (1 << 28) + 5
+    x = rng.integers(0, 8, n).astype(np.float16)
+    xd = torch.from_numpy(x).to(cuda)
+    exp = O.ref_seg_reduce(x, s)
+    got32 = D.seg_reduce(xd, s, torch.float32).cpu().numpy()
+    assert np.array_equal(got32, exp.astype(np.float32))
+    got16 = D.seg_reduce(xd, s, torch.float16).cpu().numpy()
+    assert np.array_equal(got16, exp.astype(np.float16))
