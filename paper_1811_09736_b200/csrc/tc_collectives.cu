@@ -198,7 +198,7 @@ struct Cfg {
   static constexpr bool SCAN32_2BUF = (MODE == MODE_GENERAL || MODE == MODE_IRREG);
   static constexpr int STAGES = CHUNK ? 8
                                 : (OP == OP_REDUCE)
-                                    ? ((MINB == 3 || MODE == MODE_GSCR) ? 4
+                                    ? ((MINB == 3 || MODE == MODE_GSCR || MODE == MODE_IRREG) ? 4
                                        : MINB == 2 ? 6 : 8)
                                 : (MINB == 2 && sizeof(OutT) == 4 && SCAN32_2BUF) ? 2
                                                     : (MINB == 2 ? 4 : 6);
@@ -221,7 +221,7 @@ struct Cfg {
   // GENERAL reduce with one-element granules (odd s): each thread's row of
   // granule prefixes staged in SMEM (row stride 68 floats: conflict-free
   // 16-B stores) so the row's many segment ends are one load each
-  static constexpr bool SCR = (OP == OP_REDUCE && MODE == MODE_GSCR);
+  static constexpr bool SCR = (OP == OP_REDUCE && (MODE == MODE_GSCR || MODE == MODE_IRREG));
   static constexpr uint32_t SCR_BYTES = SCR ? kTileRows * 68 * 4 : 0;
   static constexpr uint32_t OFF_SCR = OFF_OUT + OUT_BUFS * OUT_BYTES;
   static constexpr uint32_t OFF_MISC = OFF_SCR + SCR_BYTES;
@@ -251,6 +251,8 @@ struct Misc {
   int apf[2][4];
   double apd[2][4];
   int icnt[2][kTileRows];  // IRREG: segment starts per row of the tile (double-buffered)
+  double irs[kTileRows + 1];  // IRREG reduce: exclusive fp64 prefix of the tile's row totals
+  double irw[2][4];           // IRREG reduce: per-warp row-total sums
   double idv[4];           // IRREG scan: carry-in composition scratch
   int idf[4];
   uint64_t pfull[4];   // CHUNK: prefix warp -> epilogue (entry value of unit j ready)
@@ -1003,7 +1005,10 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
     auto ld_off = [&](long long k) -> long long {
       return k <= p.nseg ? __ldg(p.offs + k) : kNoStart;
     };
-    auto irreg_rows = [&](long long t, int par, long long& lo, long long& hi) -> long long {
+    // (the reduce only needs the tile's start range [tk0, tk1): no per-row counts)
+    auto irreg_rows = [&](long long t, int par, long long& lo, long long& hi, long long& tk0,
+                          long long& tk1) -> long long {
+      constexpr bool kRowsNeeded = (OP == OP_SCAN);
       const long long tb = t * kTileElems;
       const long long te = (t == T - 1) ? kNoStart - 1 : tb + kTileElems;
       int* cnt = misc->icnt[par];
@@ -1016,7 +1021,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
                             : (pf_ok && round == 1) ? pf1
                                                     : ld_off(kb + et);
         const bool in = o < te;
-        if (in) {
+        if (kRowsNeeded && in) {
           long long rr = (o - tb) >> 6;
           rr = rr < 0 ? 0 : (rr > kTileRows - 1 ? kTileRows - 1 : rr);
           atomicAdd(&cnt[rr], 1);
@@ -1037,9 +1042,12 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
       // rows = the warp's inclusive scan + the rows of the lower warps, read
       // straight from smem (no further barrier)
       const long long tile_starts = kb - kc;  // uniform
-      if (tile_starts == 0) {
+      tk0 = kc;
+      tk1 = kb;
+      if (tile_starts == 0 || !kRowsNeeded) {
         lo = hi = kc;
-        return 0;
+        kc = kb;
+        return tile_starts;
       }
       const int cr = cnt[rit];
       int incl = cr;
@@ -1285,7 +1293,8 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
         // IRREG: segment starts of this row, [i_lo, i_hi) in offs (before the
         // TMEM wait, so the offset loads overlap the MMA)
         long long i_lo = 0, i_hi = 0, i_tn = 1;  // i_tn: segment starts in the tile (uniform)
-        if constexpr (C::IRREG) i_tn = irreg_rows(t, par, i_lo, i_hi);
+        long long i_k0 = 0, i_k1 = 0;            // the tile's starts: offsets [i_k0, i_k1)
+        if constexpr (C::IRREG) i_tn = irreg_rows(t, par, i_lo, i_hi, i_k0, i_k1);
         if (wait_full) ptx::mbar_wait_warp(&misc->tfull[a], aph);
         ptx::tc_fence_after();
         constexpr int LD = C::LD_COLS;
@@ -1322,47 +1331,68 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
                                          (misc->pv[par][2] + misc->pv[par][3]));
             return;
           }
+          // segment-centric: the tile's row prefixes go to SMEM once, the
+          // row totals get an fp64 tile-level exclusive prefix R, and then
+          // thread i sums segments kc + i, kc + i + 128, ... that start and
+          // end inside the tile (coalesced offset loads and output stores,
+          // no per-row loops).  G(p) = R[p/64] + P_row(p%64) is the tile
+          // prefix at position p; a segment inside one row is P(b) - P(a)
+          // in fp32, a longer one (R[rb] - R[ra]) + P(b) - P(a) in fp64.
           OutT* out = reinterpret_cast<OutT*>(p.out);
-          const long long rowbase = row * kRow;
-          const int seen = (i_hi > i_lo) ? 1 : 0;
-          float head = 0.f, run = vv[63];
-          if (seen) {
-            float pb = row_prefix(vv, irreg_pos(__ldg(p.offs + i_lo) - rowbase));
-            head = pb;
-            for (long long k = i_lo; k + 1 < i_hi; ++k) {
-              const float p2 = row_prefix(vv, irreg_pos(__ldg(p.offs + k + 1) - rowbase));
-              out[k] = cvt_out<OutT>(p2 - pb);
-              pb = p2;
-            }
-            run = vv[63] - pb;
+          float* scr0 = reinterpret_cast<float*>(smem + C::OFF_SCR);
+          {
+            float* scr = scr0 + rit * 68;
+  #pragma unroll
+            for (int j = 0; j < 16; ++j)
+              *reinterpret_cast<float4*>(scr + 4 * j) =
+                  make_float4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]);
           }
-          float v = run;
-          int f = seen;
-          warp_pair_scan(v, f, lane);
-          float ve = __shfl_up_sync(kFull, v, 1);
-          int fe = __shfl_up_sync(kFull, f, 1);
-          if (lane == 0) {
-            ve = 0.f;
-            fe = 0;
+          const double tr = static_cast<double>(vv[63]);
+          double incl = tr;
+  #pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const double u = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += u;
           }
-          if (lane == 31) {
-            misc->pv[par][qd] = v;
-            misc->pf[par][qd] = f;
-          }
+          if (lane == 31) misc->irw[par][qd] = incl;
           ptx::named_bar_sync(kEpiBar, kEpiThreads);
-          float wv = 0.f, tv = 0.f;
-          int wf = 0, tf = 0;
-#pragma unroll
+          double woff = 0.0, wtot = 0.0;
+  #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const float yv = misc->pv[par][k];
-            const int yf = misc->pf[par][k];
-            if (k < qd) compose(wv, wf, yv, yf);
-            compose(tv, tf, yv, yf);
+            const double y = misc->irw[par][k];
+            if (k < qd) woff += y;
+            wtot += y;
           }
-          compose(wv, wf, ve, fe);
-          const long long seg0 = i_lo - 1;
-          if (seen && seg0 >= 0) {
-            const double val = static_cast<double>(wv + head) + (wf ? 0.0 : carry);
+          misc->irs[rit] = woff + (incl - tr);
+          if (et == kEpiThreads - 1) misc->irs[kTileRows] = wtot;
+          ptx::named_bar_sync(kEpiBar, kEpiThreads);
+          const long long tb = t * kTileElems;
+          auto tpos = [&](long long o) -> int {  // position in the tile, clamped to [0, 8192]
+            const long long q = o - tb;
+            return static_cast<int>(q < 0 ? 0 : (q > kTileElems ? kTileElems : q));
+          };
+          auto prow = [&](int q) -> float {  // in-row prefix before position q
+            const int c = q & 63;
+            return c ? scr0[(q >> 6) * 68 + c - 1] : 0.f;
+          };
+          auto gpos = [&](int q) -> double { return misc->irs[q >> 6] + static_cast<double>(prow(q)); };
+          for (long long k = i_k0 + et; k + 1 < i_k1; k += kEpiThreads) {
+            const int qa = tpos(__ldg(p.offs + k)), qb = tpos(__ldg(p.offs + k + 1));
+            if ((qa >> 6) == (qb >> 6)) {
+              out[k] = cvt_out<OutT>(prow(qb) - prow(qa));
+            } else {
+              const double v = (misc->irs[qb >> 6] - misc->irs[qa >> 6]) +
+                               (static_cast<double>(prow(qb)) - static_cast<double>(prow(qa)));
+              out[k] = cvt_out_d<OutT>(v);
+            }
+          }
+          // the tile's first start closes segment i_k0 - 1 (carry + head);
+          // the segment of its last start stays open (carry = tail)
+          const double head = gpos(tpos(__ldg(p.offs + i_k0)));
+          const double tail = misc->irs[kTileRows] - gpos(tpos(__ldg(p.offs + i_k1 - 1)));
+          const long long seg0 = i_k0 - 1;
+          if (seg0 >= 0 && leader) {
+            const double val = carry + head;
             if (seg0 < krange0) {
               misc->head_seg = seg0;  // partial: segment began in an earlier CTA's range
               misc->head_val = val;
@@ -1370,7 +1400,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
               out[seg0] = cvt_out_d<OutT>(val);
             }
           }
-          carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
+          carry = tail;
         } else if constexpr (OP == OP_REDUCE) {
           // ================================================= reduce
           float gs[GR];
