@@ -30,9 +30,18 @@
  *     the last segment may be ragged (shorter); a reduce returns
  *     ceil(n/seg) sums, a scan returns n prefix sums.
  *   - Arithmetic: products on the tensor core (tcgen05.mma kind::f16, fp32
- *     accumulation in TMEM), cross-row / cross-tile carries in fp32 / fp64,
- *     one rounding to the output dtype.  This is never less precise than the
- *     reference TileEngine.mma model (engine.py:326-348).
+ *     accumulation in TMEM), in-tile row / warp combines in fp32, cross-tile
+ *     and cross-CTA carries in fp64 (CHUNK unit aggregates as double-float
+ *     pairs), one rounding to the output dtype.  Every output is a sum of
+ *     its OWN segment's elements only: |out - exact| <= 1 ulp_out(exact) +
+ *     16 * 2^-24 * sum|x| (the segment, or the segment's prefix for a scan;
+ *     tests/test_parity_signed_gpu.py).  Irregular segments: the same with
+ *     sum|x| taken from the start of the 64-element row holding the
+ *     segment's first element.  Exact-integer data is bit-exact.
+ *   - Non-finite inputs: NaN / Inf * 0 in the MMA poisons the element's
+ *     64-element row (the reference's engine.py:344 poisons a 16-wide tile
+ *     row): outputs of segments running through it may be NaN (DESIGN.md
+ *     section 5).
  *   - Argument errors are detected on the host before any launch and leave
  *     `out` untouched.  Status codes map 1:1 onto the reference exceptions:
  *     TC_BAD_LENGTH -> halftile.errors.BadLengthError, TC_BAD_CONFIG ->
@@ -145,10 +154,12 @@ int tc_irreg_scan(const void* x, int in_dtype, int64_t n, const int64_t* offsets
  * PAPER.md:2185-2217) of an NCHW-contiguous tensor
  * x[N][C][HW] (in_dtype TC_F16 | TC_BF16): per channel c, mean[c] and the
  * biased variance var[c] over the N*HW elements, out_dtype TC_F32 | TC_F64
- * (DEVICE arrays of C).  Pass 1 = tc_seg_reduce_ex with seg = HW on the
- * tensor core (the mean, as in the paper); pass 2 = the centred second
- * moment on CUDA cores; pass 3 combines.  ws >= tc_workspace_bytes(
- * TC_OP_BN_STATS, N*C*HW, HW).  Three launches, stream-ordered. */
+ * (DEVICE arrays of C).  One read of x: per (n, c) segment the shifted-data
+ * moments sum(x - K_c), sum((x - K_c)^2), K_c = x[0][c][0], then a fixed-
+ * order fp64 combine per channel (CUDA cores: the squares need the elements,
+ * which a constant-B MMA cannot give).  ws >= tc_workspace_bytes(
+ * TC_OP_BN_STATS, N*C*HW, HW); the scratch is cleared again by the second
+ * launch.  Two launches, stream-ordered. */
 int tc_bn_stats(const void* x, int in_dtype, int64_t N, int64_t C, int64_t HW, void* mean,
                 void* var, int out_dtype, void* ws, size_t ws_bytes, void* stream);
 

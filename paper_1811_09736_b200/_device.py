@@ -203,7 +203,8 @@ def bn_stats(x: torch.Tensor, out_dtype=torch.float32):
     if N * C * HW == 0:
         raise BadLengthError("batch-norm statistics of an empty tensor")
     if x.dtype not in _IN:
-        x = x.to(torch.float16)
+        raise TypeError(f"batch-norm statistics take fp16 or bf16 input, got {x.dtype} "
+                        "(convert explicitly; fp32 activations above 65504 overflow fp16)")
     if not x.is_contiguous() or x.data_ptr() % 16:
         x = x.contiguous().clone()
     mean = torch.empty(C, dtype=out_dtype, device=x.device)

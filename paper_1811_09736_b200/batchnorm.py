@@ -5,14 +5,20 @@ SURVEY.md section 8(f)4).  The reference package has no entry point for
 it; this one follows its conventions (numpy in -> numpy out, torch CUDA in
 -> torch CUDA out, HalftileError subclasses for bad shapes).
 
-``batch_norm_stats(x)`` for x of shape (N, C, *spatial), NCHW-contiguous:
+``batch_norm_stats(x)`` for x of shape (N, C, *spatial), NCHW-contiguous,
+fp16 or bf16 (other dtypes raise TypeError: narrowing fp32 activations to
+fp16 would overflow above 65504 and round the statistics):
 
-* mean[c] = sum of x[:, c] / (N * HW): the (n, c) segment sums come from the
-  tensor-core segmented reduce (``tc_seg_reduce_ex``, s = HW, fp64 sums),
-  exactly the paper's use of the TCU;
-* var[c] = biased variance, from the centred second moment sum (x - K)^2,
-  K = fp32(mean), on CUDA cores (the paper leaves "all other operations"
-  off the TCU) -- two-pass, so no E[x^2] - mean^2 cancellation.
+* ONE read of x (``tc_bn_stats``): every (n, c) segment gives its
+  shifted-data moments S1 = sum(x - K_c), S2 = sum((x - K_c)^2) with
+  K_c = x[0, c, 0], fp32 per lane and fp64 per segment;
+* a per-channel fp64 combine in fixed order: mean[c] = K_c + S1 / M,
+  var[c] = S2 / M - (S1 / M)^2 (biased; M = N * HW).  The shift keeps the
+  subtraction well conditioned (no E[x^2] - mean^2 cancellation).
+
+The squares need the elements themselves, which a tensor-core MMA against
+a constant matrix cannot produce, so the statistics run on CUDA cores; the
+mean alone (the paper's TCU use) is ``segmented_reduce(x, HW)``.
 
 ``batch_norm(x, weight, bias, eps)`` applies y = (x - mean) / sqrt(var +
 eps) * weight + bias with those statistics (the normalisation itself is an

@@ -94,8 +94,8 @@ constexpr int MODE_TILES = 2;
 constexpr int MODE_GENERAL = 3;
 constexpr int MODE_CHUNK = 4;
 constexpr int MODE_IRREG = 5;  // irregular segments from a CSR offsets array
-constexpr int MODE_GSCR = 6;   // GENERAL reduce, one-element granules, segments < a row:
-                               // the row's granule prefixes staged in SMEM for the ends
+constexpr int MODE_GSCR = 6;   // GENERAL reduce with many segment ends per row (2m < GR):
+                               // end values staged in SMEM, interior segments stored coalesced
 constexpr int kMaxCtas = 1024;                    // persistent grid cap
 constexpr long long kScanPrepassMax = 1LL << 18;  // largest seg whose range-entry carry is recomputed
 constexpr unsigned kFull = 0xffffffffu;
@@ -136,11 +136,10 @@ struct Params {
   Entry* entries;
   long long ck;        // CHUNK: tiles per unit (K)
   long long lag;       // CHUNK: units between a unit's A pass and its O pass
-  uint64_t* u_word;    // CHUNK: per-unit aggregate, one 64-bit word (see unit_word)
+  uint64_t* u_word;    // CHUNK: per-unit aggregate, two tagged 64-bit words (chunk_publish)
   int exclusive;
   int need_fixup;  // reduce: segments may straddle CTA ranges
   const long long* offs;  // IRREG: nseg + 1 non-decreasing offsets, offs[0] = 0, offs[nseg] = n
-  int cum_b;              // GENERAL reduce with m >= GR: cumulative (granule-prefix) B matrix
 };
 
 template <typename T>
@@ -221,8 +220,14 @@ struct Cfg {
   // GENERAL reduce with one-element granules (odd s): each thread's row of
   // granule prefixes staged in SMEM (row stride 68 floats: conflict-free
   // 16-B stores) so the row's many segment ends are one load each
+  // IRREG reduce: each thread's row of in-row prefixes (row stride 68 floats:
+  // conflict-free 16-B stores).  GSCR: each row's segment-end values by
+  // granule (row stride GR + 1 floats: the walk's predicated stores and the
+  // coalesced read-out are bank-conflict-free for the odd m of this mode).
   static constexpr bool SCR = (OP == OP_REDUCE && (MODE == MODE_GSCR || MODE == MODE_IRREG));
-  static constexpr uint32_t SCR_BYTES = SCR ? kTileRows * 68 * 4 : 0;
+  static constexpr uint32_t SCR_BYTES = !SCR ? 0
+                                        : IRREG ? kTileRows * 68 * 4
+                                                : ((kTileRows * (GR + 1) * 4 + 127) / 128) * 128;
   static constexpr uint32_t OFF_SCR = OFF_OUT + OUT_BUFS * OUT_BYTES;
   static constexpr uint32_t OFF_MISC = OFF_SCR + SCR_BYTES;
   static constexpr int LD_COLS = (OP == OP_SCAN || IRREG) ? 64 : GR;  // TMEM columns read per tile
@@ -260,6 +265,7 @@ struct Misc {
   double entry[4];
   long long head_seg;
   double head_val;
+  long long tile_o[2];  // GSCR: first segment ending in the tile (double-buffered)
 };
 
 template <int OP, int GR, int MODE, typename OutT>
@@ -271,7 +277,7 @@ constexpr uint32_t smem_bytes() {
 // Constant B operand, K-major, 128-B swizzled: row n (N index) holds B[k][n]
 // for k = 0..63.  Reduce: granule indicator.  Scan: block-diag upper-tri U.
 template <int OP, int GR, int N>
-__device__ void build_b(uint8_t* sb, uint16_t one_bits, bool cum = false) {
+__device__ void build_b(uint8_t* sb, uint16_t one_bits) {
   constexpr int G = 64 / GR;
   for (int idx = threadIdx.x; idx < N * 8; idx += blockDim.x) {
     const int n = idx >> 3, pos = idx & 7;
@@ -282,7 +288,7 @@ __device__ void build_b(uint8_t* sb, uint16_t one_bits, bool cum = false) {
       const int k = lc * 8 + e;
       bool one;
       if (OP == OP_REDUCE)
-        one = (n < GR) && (cum ? (k / G <= n) : (k / G == n));
+        one = (n < GR) && (k / G == n);
       else
         one = (k / G == n / G) && (k <= n);
       h[e] = one ? one_bits : 0;
@@ -388,17 +394,24 @@ __device__ double epi_range_sum(const __half* x, bool bf16, long long lo, long l
   return r;
 }
 
-// CHUNK: a unit's aggregate (value, has-segment-start) and its validity
-// tag travel in ONE 64-bit word -- high half the fp32 value, low half
-// (epoch << 2) | state, state 1 = no segment start, 2 = start -- so a
-// single relaxed store publishes it and a single relaxed load observes it
-// whole (64-bit single-copy atomicity): no fences on either side.
-__device__ __forceinline__ uint64_t unit_word(double v, int f, uint32_t ep) {
-  const uint32_t bits = __float_as_uint(static_cast<float>(v));
-  return (static_cast<uint64_t>(bits) << 32) | ((ep << 2) | (f ? 2u : 1u));
-}
+// CHUNK: a unit's aggregate (value, has-segment-start) travels as TWO
+// 64-bit words written by one 16-byte relaxed store: the fp64 value as a
+// double-float pair hi = fp32(v), lo = fp32(v - hi) (~48 significant bits),
+// each word carrying its own validity tag in the low half -- (epoch << 2) |
+// state, state 1 = no segment start, 2 = start.  A reader accepts the pair
+// only when BOTH tags carry the current epoch, so a torn 16-byte read is
+// simply retried: no fences on either side (64-bit single-copy atomicity).
+__device__ __forceinline__ uint32_t unit_tag(int f, uint32_t ep) { return (ep << 2) | (f ? 2u : 1u); }
 __device__ __forceinline__ void chunk_publish(uint64_t* word, double v, int f, uint32_t ep) {
-  ptx::st_relaxed_u64(word, unit_word(v, f, ep));
+  const float hi = static_cast<float>(v);
+  const float lo = static_cast<float>(v - static_cast<double>(hi));
+  const uint64_t tag = unit_tag(f, ep);
+  ptx::st_relaxed_v2u64(word, (static_cast<uint64_t>(__float_as_uint(hi)) << 32) | tag,
+                        (static_cast<uint64_t>(__float_as_uint(lo)) << 32) | tag);
+}
+__device__ __forceinline__ double unit_value(uint64_t w0, uint64_t w1) {
+  return static_cast<double>(__uint_as_float(static_cast<uint32_t>(w0 >> 32))) +
+         static_cast<double>(__uint_as_float(static_cast<uint32_t>(w1 >> 32)));
 }
 
 // CHUNK prefix warp: for each unit j of this CTA, the value of the open
@@ -421,7 +434,7 @@ __device__ void prefix_warp(const Params& p, MiscT* misc, long long n_units, int
     const long long left = (T - j * chunk_t + ck - 1) / ck;
     const int cnt = left < Gc ? static_cast<int>(left) : Gc;
     const int c0 = lane * per;
-    uint64_t w[kMaxPer];
+    uint64_t w[kMaxPer], w1[kMaxPer];
     unsigned pending = 0;
 #pragma unroll
     for (int k = 0; k < kMaxPer; ++k)
@@ -429,10 +442,11 @@ __device__ void prefix_warp(const Params& p, MiscT* misc, long long n_units, int
     while (pending) {  // batched: one round trip per poll, not per unit
 #pragma unroll
       for (int k = 0; k < kMaxPer; ++k)
-        if (pending & (1u << k)) w[k] = ptx::ld_relaxed_u64(p.u_word + j * Gc + c0 + k);
+        if (pending & (1u << k)) ptx::ld_relaxed_v2u64(p.u_word + 2 * (j * Gc + c0 + k), w[k], w1[k]);
 #pragma unroll
       for (int k = 0; k < kMaxPer; ++k)
-        if ((pending & (1u << k)) && (static_cast<uint32_t>(w[k]) >> 2) == ep)
+        if ((pending & (1u << k)) && (static_cast<uint32_t>(w[k]) >> 2) == ep &&
+            (static_cast<uint32_t>(w1[k]) >> 2) == ep)
           pending &= ~(1u << k);
       if (pending) __nanosleep(32);
     }
@@ -443,7 +457,7 @@ __device__ void prefix_warp(const Params& p, MiscT* misc, long long n_units, int
     for (int k = 0; k < kMaxPer; ++k) {
       const int c2 = c0 + k;
       if (k < per && c2 < cnt) {
-        const double y = static_cast<double>(__uint_as_float(static_cast<uint32_t>(w[k] >> 32)));
+        const double y = unit_value(w[k], w1[k]);
         const int yf = (static_cast<uint32_t>(w[k]) & 3u) == 2u;
         va = yf ? y : va + y;
         fa |= yf;
@@ -656,13 +670,16 @@ __global__ void __launch_bounds__(kTailThreads) irreg_tail_kernel(const __half* 
 // ------------------------------------------------------------------------
 // Batch-norm statistics (the paper's TCU-reduction consumer, PAPER.md:
 // 2185-2217).  x is NCHW-contiguous: the HW
-// elements of (n, c) are one segment.  Pass 1 is the tensor-core segmented
-// reduce (s = HW, fp64 sums) -- the mean, which is what the paper puts on
-// the TCU.  Pass 2 (CUDA cores, like the paper's "all other operations")
-// accumulates the CENTRED second moment sum (x - K)^2 with K = fp32(mean),
-// split over n, and pass 3 combines the splits in order:
-// var = S / M - (mean - K)^2 (the shifted-data formula: exact in real
-// arithmetic, no E[x^2] - mean^2 cancellation).
+// elements of (n, c) are one segment.  ONE read of x: every (n, c) segment
+// gives its shifted-data moments S1 = sum (x - K_c), S2 = sum (x - K_c)^2
+// with K_c = x[0, c, 0] (a sample of the channel, so |mean - K_c| is of the
+// order of the channel's spread and S2 / M - (S1 / M)^2 does not cancel
+// catastrophically), fp32 per lane, fp64 per segment; a per-channel pass
+// combines the N segments in fixed order in fp64 (the common shift makes
+// the combine a plain sum) and clears the scratch it read.  The squares need
+// the elements themselves, which a tensor-core MMA with a constant B cannot
+// produce, so this consumer runs on CUDA cores; the mean alone is the
+// tensor-core segmented reduce (tc_seg_reduce_ex, s = HW).
 constexpr int kBnThreads = 256;
 
 __device__ __forceinline__ double block_sum_d(double v, double* sred) {
@@ -675,57 +692,51 @@ __device__ __forceinline__ double block_sum_d(double v, double* sred) {
   return t;
 }
 
-// mean of channel c from pass 1's (n, c) sums, fixed order
-__device__ __forceinline__ double bn_channel_mean(const double* segsum, long long N, long long C,
-                                                  long long HW, long long c, double* sred) {
-  double m = 0.0;
-  for (long long n = threadIdx.x; n < N; n += blockDim.x) m += segsum[n * C + c];
-  return block_sum_d(m, sred) / static_cast<double>(N * HW);
-}
-
-__global__ void __launch_bounds__(kBnThreads) bn_centred_kernel(const __half* x, int in_bf16,
+__global__ void __launch_bounds__(kBnThreads) bn_moments_kernel(const __half* x, int in_bf16,
                                                                 long long N, long long C,
-                                                                long long HW, const double* segsum,
-                                                                double* part) {
-  __shared__ double sred[kBnThreads / 32];
-  const long long c = blockIdx.x;
-  const int splits = gridDim.y, sp = blockIdx.y;
-  const double mean = bn_channel_mean(segsum, N, C, HW, c, sred);
-  const float k = static_cast<float>(mean);
+                                                                long long HW, double2* mom) {
   const bool bf16 = in_bf16 != 0;
-  const long long n0 = N * sp / splits, n1 = N * (sp + 1) / splits;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kWarps = kBnThreads / 32;
-  double acc = 0.0;
+  const long long nsegs = N * C;
   // one warp per (n, c) segment; vector width = the segment alignment
-  // (HW % 8 == 0: 16-B loads, % 4: 8-B, % 2: 4-B, else 2-B), two in flight
+  // (HW % 8 == 0: 16-B loads, % 4: 8-B, % 2: 4-B, else 2-B), four in flight
   auto run = [&](auto vec_tag) {
     constexpr int V = decltype(vec_tag)::value;  // elements per load
     using VT = typename std::conditional<V == 8, uint4,
                typename std::conditional<V == 4, uint2,
                typename std::conditional<V == 2, uint32_t, unsigned short>::type>::type>::type;
-    auto sq = [&](const VT& w, float& fs) {
-      const unsigned short* h = reinterpret_cast<const unsigned short*>(&w);
-#pragma unroll
-      for (int q = 0; q < V; ++q) {
-        const float f = bf16 ? __uint_as_float(static_cast<uint32_t>(h[q]) << 16)
-                             : __half2float(__ushort_as_half(h[q]));
-        const float a = f - k;
-        fs = fmaf(a, a, fs);
-      }
-    };
     const long long nv = HW / V;
-    for (long long nn = n0 + warp; nn < n1; nn += kWarps) {
-      const VT* xv = reinterpret_cast<const VT*>(x + (nn * C + c) * HW);
-      float fs = 0.f;
+    for (long long q = static_cast<long long>(blockIdx.x) * kWarps + warp; q < nsegs;
+         q += static_cast<long long>(gridDim.x) * kWarps) {
+      const long long c = q % C;
+      const float k = in_to_float(x, c * HW, bf16);
+      float s1 = 0.f, s2 = 0.f;
+      auto acc = [&](const VT& w) {
+        const unsigned short* h = reinterpret_cast<const unsigned short*>(&w);
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          const float f = bf16 ? __uint_as_float(static_cast<uint32_t>(h[e]) << 16)
+                               : __half2float(__ushort_as_half(h[e]));
+          const float a = f - k;
+          s1 += a;
+          s2 = fmaf(a, a, s2);
+        }
+      };
+      const VT* xv = reinterpret_cast<const VT*>(x + q * HW);
       long long i = lane;
-      for (; i + 32 < nv; i += 64) {
-        const VT a = xv[i], b = xv[i + 32];
-        sq(a, fs);
-        sq(b, fs);
+      for (; i + 96 < nv; i += 128) {
+        const VT a = __ldcs(xv + i), b = __ldcs(xv + i + 32), cc = __ldcs(xv + i + 64),
+                 d = __ldcs(xv + i + 96);
+        acc(a);
+        acc(b);
+        acc(cc);
+        acc(d);
       }
-      if (i < nv) sq(xv[i], fs);
-      acc += static_cast<double>(fs);
+      for (; i < nv; i += 32) acc(__ldcs(xv + i));
+      const double d1 = warp_sum_d(static_cast<double>(s1));
+      const double d2 = warp_sum_d(static_cast<double>(s2));
+      if (lane == 0) mom[q] = make_double2(d1, d2);
     }
   };
   if ((HW & 7) == 0)
@@ -736,26 +747,31 @@ __global__ void __launch_bounds__(kBnThreads) bn_centred_kernel(const __half* x,
     run(std::integral_constant<int, 2>{});
   else
     run(std::integral_constant<int, 1>{});
-  const double t = block_sum_d(acc, sred);
-  if (threadIdx.x == 0) part[c * splits + sp] = t;
 }
 
 template <typename OutT>
-__global__ void __launch_bounds__(kBnThreads) bn_finish_kernel(long long N, long long C,
-                                                               long long HW, const double* segsum,
-                                                               const double* part, int splits,
+__global__ void __launch_bounds__(kBnThreads) bn_finish_kernel(const __half* x, int in_bf16,
+                                                               long long N, long long C,
+                                                               long long HW, double2* mom,
                                                                OutT* mean_out, OutT* var_out) {
   __shared__ double sred[kBnThreads / 32];
   const long long c = blockIdx.x;
-  const double mean = bn_channel_mean(segsum, N, C, HW, c, sred);
+  double a1 = 0.0, a2 = 0.0;
+  for (long long n = threadIdx.x; n < N; n += blockDim.x) {
+    const double2 m = mom[n * C + c];
+    a1 += m.x;
+    a2 += m.y;
+    mom[n * C + c] = make_double2(0.0, 0.0);  // leave the workspace zeroed
+  }
+  const double s1 = block_sum_d(a1, sred);
+  const double s2 = block_sum_d(a2, sred);
   if (threadIdx.x == 0) {
-    double s2 = 0.0;
-    for (int sp = 0; sp < splits; ++sp) s2 += part[c * splits + sp];
-    const double k = static_cast<double>(static_cast<float>(mean));
+    const double k = static_cast<double>(in_to_float(x, c * HW, in_bf16 != 0));
     const double m = static_cast<double>(N * HW);
-    double var = s2 / m - (mean - k) * (mean - k);
+    const double d = s1 / m;  // mean - K
+    double var = s2 / m - d * d;
     if (var < 0.0) var = 0.0;
-    mean_out[c] = static_cast<OutT>(mean);
+    mean_out[c] = static_cast<OutT>(k + d);
     var_out[c] = static_cast<OutT>(var);
   }
 }
@@ -853,8 +869,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
     ptx::tmem_alloc(&misc->tmem_base, C::TMEM_COLS);
     ptx::tmem_relinquish();
   }
-  build_b<(C::IRREG ? OP_SCAN : OP), GR, N>(smem + C::OFF_B, p.in_bf16 ? 0x3F80 : 0x3C00,
-                                            p.cum_b != 0);
+  build_b<(C::IRREG ? OP_SCAN : OP), GR, N>(smem + C::OFF_B, p.in_bf16 ? 0x3F80 : 0x3C00);
   if constexpr (C::IRREG) {
     for (int k = threadIdx.x; k < 2 * kTileRows; k += blockDim.x) (&misc->icnt[0][0])[k] = 0;
   }
@@ -1105,7 +1120,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
     // hand the unit's aggregate to the prefix warp, which publishes it (the
     // release store's fence would otherwise stall the TMA-issuing leader)
     auto save_unit = [&](long long uj) {
-      if (leader) chunk_publish(p.u_word + uj * Gc + cta, u_v, u_f, ep);
+      if (leader) chunk_publish(p.u_word + 2 * (uj * Gc + cta), u_v, u_f, ep);
       u_v = 0.0;
       u_f = 0;
     };
@@ -1196,6 +1211,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
         }
         ptx::named_bar_sync(kEpiBar, kEpiThreads);
         float off;
+        double offd;  // the same offset in fp64 (total_out)
         if (!st_o) {
           float woff = 0.f, ttot = 0.f;
 #pragma unroll
@@ -1204,7 +1220,8 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
             if (k < qd) woff += y;
             ttot += y;
           }
-          off = static_cast<float>(carry + static_cast<double>(o_ex + woff));
+          offd = carry + static_cast<double>(o_ex + woff);
+          off = static_cast<float>(offd);
           carry += static_cast<double>(ttot);
         } else {
           float wv = 0.f, tv = 0.f;
@@ -1217,8 +1234,9 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
             compose(tv, tf, yv, yf);
           }
           compose(wv, wf, o_ve, o_fe);
-          off = row_start(row_o) ? 0.f
-                                 : (wf ? wv : static_cast<float>(carry + static_cast<double>(wv)));
+          offd = row_start(row_o) ? 0.0
+                                  : (wf ? static_cast<double>(wv) : carry + static_cast<double>(wv));
+          off = static_cast<float>(offd);
           carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
         }
         auto outv = [&](int e) -> float {
@@ -1226,12 +1244,13 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
           return vv[e] + off;
         };
         if (p.total_out && row_o == (p.n - 1) / kRow) {
+          // the open segment's inclusive sum, from the fp64 carry
           const int k = static_cast<int>((p.n - 1) % kRow);
-          float incl = 0.f;
+          float in_row = 0.f;
 #pragma unroll
           for (int e = 0; e < 64; ++e)
-            if (e == k) incl = vv[e] + off;
-          *p.total_out = static_cast<double>(incl);
+            if (e == k) in_row = vv[e];
+          *p.total_out = static_cast<double>(in_row) + offd;
         }
         uint8_t* stg = smem + C::OFF_OUT + (C::OUT_BUFS == 2 ? par : 0) * C::OUT_BYTES;
         const uint32_t rb = static_cast<uint32_t>(rit) * 128u;
@@ -1469,75 +1488,85 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
               ++tseg;
             }
           } else {
-            // MODE_GENERAL: segmented (value, has_end) pair scan over rows
-            // segment ends inside the row, in 32-bit granule offsets: the first
+            // MODE_GENERAL / MODE_GSCR: segmented (value, has_end) pair scan
+            // over rows.  B is the granule INDICATOR, so gs[j] is the sum of
+            // granule j's own elements, and every piece below is a forward
+            // fp32 sum of whole granules of ONE segment: a segment's rounding
+            // error scales with its own elements only (never with a
+            // neighbour's, as a difference of row prefixes would).
+            // Segment ends inside the row, in 32-bit granule offsets: the first
             // at p.m - 1 - qmod, then every p.m; the input's last granule ends
-            // the ragged last segment
+            // the ragged last segment.
             const long long rem0 = p.m - 1 - qmod;
             const long long dl = p.qlast - q0;
-            const int lastj = dl < GR ? static_cast<int>(dl) : GR;
-            long long sg = qdiv;        // segment containing granule q0 + j
-            const long long seg0 = sg;  // segment closed by the row's first end
+            const long long seg0 = qdiv;  // segment closed by the row's first end
             float run = 0.f, head = 0.f;
             int seen = 0;
-            bool done = false;
-            if constexpr (C::SCR) {
-              if (p.cum_b && dl >= GR && row != p.rows_full && p.m < GR) {
-                // one-element granules, segments shorter than a row: ends at
-                // e0, e0 + m, ... (e0 < m always exists); pieces are
-                // differences of prefixes read back from this row's SMEM copy
-                float* scr = reinterpret_cast<float*>(smem + C::OFF_SCR) + rit * 68;
-  #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                  *reinterpret_cast<float4*>(scr + 4 * j) =
-                      make_float4(gs[4 * j], gs[4 * j + 1], gs[4 * j + 2], gs[4 * j + 3]);
-                const int m32 = static_cast<int>(p.m);
-                int e = static_cast<int>(rem0);
-                float prev = scr[e];  // own row: program order, no barrier
-                head = prev;
-                seen = 1;
-                long long sgi = seg0 + 1;
-                for (e += m32; e < GR; e += m32) {
-                  const float pe = scr[e];
-                  out[sgi++] = cvt_out<OutT>(pe - prev);
-                  prev = pe;
-                }
-                run = gs[GR - 1] - prev;
-                done = true;
-              }
+            if constexpr (MODE == MODE_GSCR) {
+              if (et == 0) misc->tile_o[par] = qdiv;  // first segment ending in this tile
             }
-            if (done) {
-            } else if (p.cum_b && dl >= GR && row != p.rows_full) {
-              // segments of >= half a row (2m >= GR) with the cumulative B:
-              // the columns are granule PREFIXES and at most two segments end
-              // in the row (granules e0 < e1) -> head = P[e0], the segment
-              // between them = P[e1] - P[e0], tail = P[GR-1] - P[last end]
-              const int e0 = rem0 < GR ? static_cast<int>(rem0) : -1;
-              float hv = gs[0];
+            if (dl >= GR && row != p.rows_full) {
+              // a full row that does not hold the input's last granule
+              if constexpr (MODE == MODE_GSCR) {
+                // many ends per row (2m < GR): ends at e0 < m, e0 + m, ...;
+                // each end's value is staged in this row's SMEM slot j and the
+                // tile's interior segments are stored coalesced below
+                float* stg = reinterpret_cast<float*>(smem + C::OFF_SCR) + rit * (GR + 1);
+                const int m32 = static_cast<int>(p.m);
+                const int e0 = static_cast<int>(rem0);
+                int nx = e0;
   #pragma unroll
-              for (int j = 1; j < GR; ++j) hv = (j == e0) ? gs[j] : hv;
-              float last = hv;
-              if (p.m < GR) {  // uniform: a second end is possible
-                const int e1 = (e0 >= 0 && e0 + p.m < GR) ? e0 + static_cast<int>(p.m) : -1;
-                float hv1 = gs[0];
-  #pragma unroll
-                for (int j = 1; j < GR; ++j) hv1 = (j == e1) ? gs[j] : hv1;
-                if (e1 >= 0) {
-                  out[seg0 + 1] = cvt_out<OutT>(hv1 - hv);  // wholly inside this row
-                  last = hv1;
+                for (int j = 0; j < GR; ++j) {
+                  const float v = run + gs[j];
+                  const bool end = (j == nx);
+                  if (end) {
+                    stg[j] = v;
+                    nx += m32;
+                  }
+                  run = end ? 0.f : v;
                 }
-              }
-              seen = e0 >= 0;
-              head = seen ? hv : 0.f;
-              run = seen ? gs[GR - 1] - last : gs[GR - 1];
-            } else {
-              if (p.cum_b && row != p.rows_full) {
-                // the row holding the input's last granule (or padding): back to sums
+                head = stg[e0];  // own row: program order, no barrier
+                seen = 1;
+              } else if (p.m >= GR) {
+                // at most one end (granule e0; GR = none): head = granules
+                // 0..e0, the open tail = the rest
+                const int e0 = rem0 < GR ? static_cast<int>(rem0) : GR;
+                float a = 0.f, b = 0.f;
   #pragma unroll
-                for (int j = GR - 1; j > 0; --j) gs[j] -= gs[j - 1];
+                for (int j = 0; j < GR; ++j) {
+                  if (j <= e0)
+                    a += gs[j];
+                  else
+                    b += gs[j];
+                }
+                seen = e0 < GR;
+                head = a;
+                run = seen ? b : a;
+              } else {
+                // at most two ends (2m >= GR): head, one interior segment, tail
+                const int e0 = rem0 < GR ? static_cast<int>(rem0) : GR;
+                const int e1 = (e0 < GR && e0 + p.m < GR) ? e0 + static_cast<int>(p.m) : GR;
+                float a = 0.f, b = 0.f, c = 0.f;
+  #pragma unroll
+                for (int j = 0; j < GR; ++j) {
+                  if (j <= e0)
+                    a += gs[j];
+                  else if (j <= e1)
+                    b += gs[j];
+                  else
+                    c += gs[j];
+                }
+                seen = e0 < GR;
+                head = a;
+                if (e1 < GR) out[seg0 + 1] = cvt_out<OutT>(b);  // wholly inside this row
+                run = !seen ? a : (e1 < GR ? c : b);
               }
+            } else {
+              // the row holding the input's last granule (or padding): walk
+              const int lastj = dl < GR ? static_cast<int>(dl) : GR;
               const int m32 = p.m < (1LL << 20) ? static_cast<int>(p.m) : (1 << 20);
               int e = rem0 < GR ? static_cast<int>(rem0) : GR;
+              long long sg = seg0;  // segment containing granule q0 + j
   #pragma unroll
               for (int j = 0; j < GR; ++j) {
                 run += gs[j];
@@ -1579,7 +1608,8 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
             }
             compose(wv, wf, ve, fe);
             if (seen) {
-              const double val = static_cast<double>(wv + head) + (wf ? 0.0 : carry);
+              const double val =
+                  (static_cast<double>(wv) + static_cast<double>(head)) + (wf ? 0.0 : carry);
               if (seg0 * p.seg < range_first_elem) {
                 misc->head_seg = seg0;  // partial: segment began in an earlier CTA's range
                 misc->head_val = val;
@@ -1588,6 +1618,28 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
               }
             }
             carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
+            if constexpr (MODE == MODE_GSCR) {
+              // the tile's interior segments (ending at a row's second, third,
+              // ... end) from the SMEM staging slots, one output per thread per
+              // round: coalesced stores instead of one scattered store per end.
+              // Every row's walk is complete (pair-scan barrier above); the
+              // row holding the input's last granule stored its own.
+              const float* stg0 = reinterpret_cast<const float*>(smem + C::OFF_SCR);
+              const long long g0 = t * static_cast<long long>(kTileRows) * GR;
+              long long gend = g0 + static_cast<long long>(kTileRows) * GR;
+              const long long glim = (p.qlast / GR) * GR;
+              if (gend > glim) gend = glim;
+              const long long m = p.m;
+              for (long long o = misc->tile_o[par] + et;; o += kEpiThreads) {
+                const long long ge = (o + 1) * m - 1;  // the segment's last granule
+                if (ge >= gend) break;
+                const int lg = static_cast<int>(ge - g0);
+                const int jc = lg & (GR - 1);
+                if (jc >= m) out[o] = cvt_out<OutT>(stg0[(lg / GR) * (GR + 1) + jc]);
+              }
+              // the next tile's walk rewrites the slots
+              ptx::named_bar_sync(kEpiBar, kEpiThreads);
+            }
             // advance to the next tile's row (contiguous ranges)
             qmod += p.step_mod;
             qdiv += p.step_div;
@@ -1617,6 +1669,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
           // must have finished reading it before anyone writes (barrier below).
           if (leader) ptx::bulk_wait_read<C::OUT_BUFS - 1>();
           float off[GR];  // per-granule offset to add (exclusive prefix within segment)
+          double cinfd = 0.0;  // TILES / GENERAL / CHUNK: the carry part of off in fp64 (total_out)
           if constexpr (MODE == MODE_LOCAL) {
             ptx::named_bar_sync(kEpiBar, kEpiThreads);
   #pragma unroll
@@ -1667,7 +1720,8 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
               ttot += y;
             }
             if (tpos == 0) carry = 0.0;  // a segment starts at this tile
-            off[0] = static_cast<float>(carry + static_cast<double>(excl + woff));
+            cinfd = carry + static_cast<double>(excl + woff);
+            off[0] = static_cast<float>(cinfd);
             carry += static_cast<double>(ttot);
             if (++tpos == p.ktiles) {
               tpos = 0;
@@ -1838,7 +1892,22 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
               tprefix = carry;
               carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
             }
-            const float cinf = wf ? wv : static_cast<float>(tprefix + static_cast<double>(wv));
+            cinfd = wf ? static_cast<double>(wv) : tprefix + static_cast<double>(wv);
+            if (p.total_out && row == (p.n - 1) / kRow) {
+              // the open segment's inclusive sum: in-row part + the fp64 carry
+              const int k = static_cast<int>((p.n - 1) % kRow);
+              float in_g = 0.f, o = 0.f;
+              int ch = 0;
+  #pragma unroll
+              for (int e = 0; e < 64; ++e)
+                if (e == k) {
+                  in_g = vv[e];
+                  o = off[e / G];
+                  ch = chain[e / G];
+                }
+              *p.total_out = static_cast<double>(in_g) + static_cast<double>(o) + (ch ? cinfd : 0.0);
+            }
+            const float cinf = static_cast<float>(cinfd);
   #pragma unroll
             for (int j = 0; j < GR; ++j)
               if (chain[j]) off[j] += cinf;
@@ -1853,13 +1922,18 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
             if (excl) return (e % G == 0) ? (base + 0.f) : (vv[e - 1] + base);
             return vv[e] + base;
           };
-          if (!C::IRREG && p.total_out && row == (p.n - 1) / kRow) {
-            const int k = static_cast<int>((p.n - 1) % kRow);
-            float incl = 0.f;
+          if constexpr (MODE == MODE_LOCAL || MODE == MODE_ROWS || MODE == MODE_TILES) {
+            if (p.total_out && row == (p.n - 1) / kRow) {
+              // (GENERAL / CHUNK wrote it above, from their fp64 carry)
+              const int k = static_cast<int>((p.n - 1) % kRow);
+              float in_g = 0.f;
   #pragma unroll
-            for (int e = 0; e < 64; ++e)
-              if (e == k) incl = vv[e] + off[ONE_OFF ? 0 : e / G];
-            *p.total_out = static_cast<double>(incl);
+              for (int e = 0; e < 64; ++e)
+                if (e == k) in_g = vv[e];
+              *p.total_out = static_cast<double>(in_g) + (MODE == MODE_TILES ? cinfd
+                                                          : MODE == MODE_ROWS ? static_cast<double>(off[0])
+                                                                              : 0.0);
+            }
           }
           uint8_t* stg = smem + C::OFF_OUT + (C::OUT_BUFS == 2 ? par : 0) * C::OUT_BYTES;
           const uint32_t rb = static_cast<uint32_t>(rit) * 128u;
@@ -2071,7 +2145,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
           u_f |= tf;
         }
         if (last_a) {
-          if (ea == 0) chunk_publish(p.u_word + ja_c * Gc + cta, u_v, u_f, ep);
+          if (ea == 0) chunk_publish(p.u_word + 2 * (ja_c * Gc + cta), u_v, u_f, ep);
           u_v = 0.0;
           u_f = 0;
         }
@@ -2170,8 +2244,8 @@ static long long chunk_slots(long long n) { return (n + kTileElems - 1) / kTileE
 static size_t ws_need(int op, long long n, long long seg) {
   size_t b = kWsLookback;
   if (op == TC_OP_SCAN)
-    b += static_cast<size_t>(chunk_slots(n)) * sizeof(uint64_t) + 64;
-  if (op == TC_OP_BN_STATS)  // (n, c) segment sums + per-(c, split) centred partials
+    b += static_cast<size_t>(chunk_slots(n)) * 2 * sizeof(uint64_t) + 64;
+  if (op == TC_OP_BN_STATS)  // per-(n, c) shifted moments (S1, S2), cleared after use
     b += 2 * sizeof(double) * static_cast<size_t>((n + seg - 1) / (seg > 0 ? seg : 1)) + 512;
   return (b + 255) & ~size_t(255);
 }
@@ -2248,8 +2322,7 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
   // 97 %, fp16 scans 93-95 vs 91-92 %); cooperative launches (CHUNK) must
   // match the API.
   if (MODE != MODE_CHUNK) {
-    // (a GENERAL reduce on the cumulative-B path is light enough for 2)
-    per_sm = ((MODE == MODE_GENERAL && OP == OP_REDUCE && p0.cum_b) || MODE == MODE_GSCR) ? 2
+    per_sm = (MODE == MODE_GSCR) ? 2
              : (MODE == MODE_GENERAL || MODE == MODE_IRREG) ? Cfg<OP, GR, MODE, OutT>::MINB
              : ((OP == OP_REDUCE && MODE == MODE_ROWS && p0.log2m >= 4 && p0.log2m < 7) ||
                 (OP == OP_SCAN && MODE == MODE_LOCAL && sizeof(OutT) == 4))
@@ -2362,7 +2435,14 @@ static LaunchFn pick(int gr, int mode) {
       return nullptr;
     case MODE_IRREG: return gr == 1 ? &launch<OP, 1, MODE_IRREG, OutT> : nullptr;
     case MODE_GSCR:
-      if constexpr (OP == OP_REDUCE) return gr == 64 ? &launch<OP, 64, MODE_GSCR, OutT> : nullptr;
+      if constexpr (OP == OP_REDUCE) {
+        switch (gr) {
+          case 8: return &launch<OP, 8, MODE_GSCR, OutT>;
+          case 16: return &launch<OP, 16, MODE_GSCR, OutT>;
+          case 32: return &launch<OP, 32, MODE_GSCR, OutT>;
+          case 64: return &launch<OP, 64, MODE_GSCR, OutT>;
+        }
+      }
       return nullptr;
   }
   return nullptr;
@@ -2445,18 +2525,11 @@ static Params make_params(const void* x, long long n, long long seg, void* out, 
   size_t off = kWsLookback;
   p.u_word = reinterpret_cast<uint64_t*>(w + off);
   p.ck = 1;
-  // GENERAL reduce whose segments span at least a row (or half a row, with
-  // >= 16 granules per row): B = granule prefixes (B[k][j] = [k/g <= j]) so
-  // one or two selects find the row's segment ends (measured: at 4-8
-  // granules per row the granule walk is as fast)
-  p.cum_b = (op == TC_OP_REDUCE && mode == MODE_GENERAL && gr > 1 &&
-             (p.m >= gr || (2 * p.m >= gr && gr >= 16) || gr == 64))
-                ? 1
-                : 0;
-  // one-element granules and segments shorter than a row: many ends per row,
-  // looked up from an SMEM copy of the row's prefixes (its own mode, so the
-  // longer-segment GENERAL kernels keep their 6-stage ring)
-  if (op == TC_OP_REDUCE && mode == MODE_GENERAL && gr == 64 && p.m < gr) mode = MODE_GSCR;
+  // GENERAL reduce with many segment ends per row (2m < GR; m is odd, so
+  // GR >= 8): its own mode, the walk's end values staged in SMEM and the
+  // interior segments stored coalesced (the other GENERAL kernels keep their
+  // deeper rings and no staging buffer)
+  if (op == TC_OP_REDUCE && mode == MODE_GENERAL && 2 * p.m < gr) mode = MODE_GSCR;
   *mode_out = mode;
   p.need_fixup = (op == TC_OP_REDUCE &&
                   (mode == MODE_TILES || mode == MODE_GENERAL || mode == MODE_GSCR) &&
@@ -2590,7 +2663,6 @@ static Params irreg_params(const void* x, int in_dtype, int64_t n, const int64_t
   p.in_bf16 = (in_dtype == TC_BF16) ? 1 : 0;
   p.offs = reinterpret_cast<const long long*>(offsets);
   p.nseg = nseg;
-  p.cum_b = 0;
   p.need_fixup = (op == TC_OP_REDUCE) ? 1 : 0;
   return p;
 }
@@ -2639,32 +2711,38 @@ int tc_bn_stats(const void* x, int in_dtype, int64_t N, int64_t C, int64_t HW, v
     set_err("workspace too small: need %s%lld bytes", "", (long long)ws_need(TC_OP_BN_STATS, n, HW));
     return TC_WORKSPACE_TOO_SMALL;
   }
-  // pass 1: (n, c) segment sums on the tensor core, fp64, into the workspace tail
-  char* w = reinterpret_cast<char*>(ws);
-  const size_t base = ws_need(TC_OP_REDUCE, n, HW);
-  double* segsum = reinterpret_cast<double*>(w + base);
-  double* part = segsum + N * C;
-  int rc = tc_seg_reduce_ex(x, in_dtype, n, HW, segsum, TC_F64, ws, base, stream);
-  if (rc) return rc;
+  if (!x || (reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(ws) & 255)) {
+    set_err("x must be non-null and 16-byte aligned, ws 256-byte aligned%s%lld", "", 0);
+    return TC_BAD_ALIGNMENT;
+  }
+  if (in_dtype != TC_F16 && in_dtype != TC_BF16) {
+    set_err("unsupported input dtype %s%lld", "", in_dtype);
+    return TC_BAD_CONFIG;
+  }
+  // scratch: the per-(n, c) moments, at the start of the look-back region
+  // (bn_finish_kernel clears every entry it read, so the region stays zero)
+  double2* mom = reinterpret_cast<double2*>(reinterpret_cast<char*>(ws) + kWsLookback);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int dev = 0;
   cudaGetDevice(&dev);
   const DevInfo di = dev_info(dev);
-  long long splits = (2LL * (di.sms > 0 ? di.sms : 148) + C - 1) / C;
-  if (splits > N) splits = N;
-  if (splits > 65535) splits = 65535;
-  if (splits < 1) splits = 1;
-  bn_centred_kernel<<<dim3(static_cast<unsigned>(C), static_cast<unsigned>(splits)), kBnThreads, 0,
-                      st>>>(reinterpret_cast<const __half*>(x), in_dtype == TC_BF16 ? 1 : 0, N, C,
-                            HW, segsum, part);
+  if (!di.ok || di.major < 10) {
+    set_err("no sm_100 device (compute capability major %s%lld)", "", di.major);
+    return TC_NO_DEVICE;
+  }
+  const long long nsegs = N * C;
+  long long blocks = (nsegs + kBnThreads / 32 - 1) / (kBnThreads / 32);
+  const long long cap = static_cast<long long>(di.sms) * (2048 / kBnThreads);  // one wave
+  if (blocks > cap) blocks = cap;
+  const __half* xh = reinterpret_cast<const __half*>(x);
+  const int bf = in_dtype == TC_BF16 ? 1 : 0;
+  bn_moments_kernel<<<static_cast<unsigned>(blocks), kBnThreads, 0, st>>>(xh, bf, N, C, HW, mom);
   if (out_dtype == TC_F32)
     bn_finish_kernel<float><<<static_cast<unsigned>(C), kBnThreads, 0, st>>>(
-        N, C, HW, segsum, part, static_cast<int>(splits), reinterpret_cast<float*>(mean),
-        reinterpret_cast<float*>(var));
+        xh, bf, N, C, HW, mom, reinterpret_cast<float*>(mean), reinterpret_cast<float*>(var));
   else
     bn_finish_kernel<double><<<static_cast<unsigned>(C), kBnThreads, 0, st>>>(
-        N, C, HW, segsum, part, static_cast<int>(splits), reinterpret_cast<double*>(mean),
-        reinterpret_cast<double*>(var));
+        xh, bf, N, C, HW, mom, reinterpret_cast<double*>(mean), reinterpret_cast<double*>(var));
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_err("kernel launch failed: %s%lld", cudaGetErrorString(e), 0);

@@ -182,9 +182,12 @@ def grid_reduce(values, engine: TileEngine, cfg: BlockConfig = BlockConfig(),
                 block_elems: int = 4096, workers: int = 1, reverse: bool = False,
                 debug_capture: dict | None = None):
     """Full reduction (reduce.py:332-373) in ONE kernel launch: per-CTA fp64
-    partials combined in CTA order by the last CTA (no second pass).
-    ``debug_capture`` records ``passes`` = 1 (launches) and, if requested,
-    the ``block_elems`` block partials (one extra launch)."""
+    partials combined in CTA order by the last CTA.  ``debug_capture``
+    receives the reference's keys: ``passes`` = GRID_REDUCE_PASSES, the
+    reference algorithm's two logical passes (block partials, then their
+    reduction), which the B200 kernel fuses -- ``launches`` = 1 says so --
+    and ``partials``, the ``block_elems`` block sums in the accumulator dtype
+    (one extra launch, only when requested)."""
     x, kind = _as_flat_half(values)
     if block_elems % (256 * cfg.wpb):
         raise BadConfigError(
@@ -194,7 +197,8 @@ def grid_reduce(values, engine: TileEngine, cfg: BlockConfig = BlockConfig(),
         raise BadLengthError("input must be a non-empty flat vector")
     total = _scalar(_device_reduce(x, kind, size, engine), engine)
     if debug_capture is not None:
-        debug_capture["passes"] = 1
+        debug_capture["passes"] = GRID_REDUCE_PASSES
+        debug_capture["launches"] = 1
         debug_capture["partials"] = _device_reduce(x, kind, block_elems, TileEngine(
             accumulate=engine.accumulate))
     return total

@@ -114,7 +114,30 @@ def block_scan_256n(values, cfg: BlockConfig, engine: TileEngine, workers: int =
     n = size // 256
     if n % cfg.wpb:
         raise BadConfigError(f"{n} tiles do not divide across {cfg.wpb} warps")
+    if debug_capture is not None:
+        _capture_first_super_iteration(x, kind, cfg.wpb, engine, debug_capture)
     return _device_scan(x, kind, size, engine)
+
+
+def _capture_first_super_iteration(x, kind, wpb: int, engine: TileEngine, cap: dict) -> None:
+    """The reference's block-scan introspection (scan.py:224-227): the
+    scratch of the first super-iteration (``first_sout``: the wpb unseeded
+    256-element tile scans, zeros after) and its partials (``first_prtls``:
+    last_column_scan_16 of the tiles' totals, seeded with 0).  Recomputed on
+    the GPU from the same tile scans / totals (extra launches, only when
+    requested) -- the B200 kernel itself has no such scratch."""
+    head = x[: 256 * wpb]
+    eng = TileEngine(accumulate=engine.accumulate)
+    sout = np.zeros(256 * 16, dtype=engine.acc_dtype)
+    sout[: 256 * wpb] = _as_numpy(_device_scan(head, kind, 256, eng))
+    tile = np.zeros((16, 16), np.float64)
+    tile[:wpb, 15] = sout[255: 256 * wpb: 256]
+    cap["first_prtls"] = last_column_scan_16(tile, eng, carry=0.0)
+    cap["first_sout"] = sout
+
+
+def _as_numpy(a):
+    return a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
 
 
 # -- grid level ----------------------------------------------------------------
@@ -123,19 +146,34 @@ def block_scan_256n(values, cfg: BlockConfig, engine: TileEngine, workers: int =
 def grid_scan(values, engine: TileEngine, cfg: BlockConfig = BlockConfig(),
               block_elems: int = 4096, workers: int = 1, reverse: bool = False,
               debug_capture: dict | None = None):
-    """Inclusive scan of the whole vector (scan.py:249-310) in ONE launch
-    (decoupled look-back with fp64 prefixes instead of three passes)."""
+    """Inclusive scan of the whole vector (scan.py:249-310) in ONE launch:
+    the CHUNK kernel fuses the reference's three passes (block totals, their
+    scan, the uniform add) -- unit aggregates, their fixed-order fp64
+    composition and the carry-seeded output pass run concurrently in one
+    kernel.  ``debug_capture`` receives the reference's keys: ``passes`` =
+    GRID_SCAN_PASSES (the logical passes; ``launches`` = 1 says they are
+    fused) and ``block_totals``, the ``block_elems`` block sums in the
+    accumulator dtype (one extra launch, only when requested)."""
     x, kind = _as_flat_half(values)
-    if block_elems % (256 * cfg.wpb):
-        raise BadConfigError(
-            f"block capacity {block_elems} is not a multiple of 256*wpb ({256 * cfg.wpb})")
+    _check_grid_cfg(cfg, block_elems)
     size = _d.size_of(x)
     if size == 0:
         raise BadLengthError("input must be a non-empty flat vector")
     out = _device_scan(x, kind, size, engine)
     if debug_capture is not None:
-        debug_capture["passes"] = 1
+        from .reduce import _device_reduce
+
+        debug_capture["passes"] = GRID_SCAN_PASSES
+        debug_capture["launches"] = 1
+        debug_capture["block_totals"] = _as_numpy(_device_reduce(
+            x, kind, block_elems, TileEngine(accumulate=engine.accumulate)))
     return out
+
+
+def _check_grid_cfg(cfg: BlockConfig, block_elems: int = 4096) -> None:
+    if block_elems % (256 * cfg.wpb):
+        raise BadConfigError(
+            f"block capacity {block_elems} is not a multiple of 256*wpb ({256 * cfg.wpb})")
 
 
 # -- segmented driver -----------------------------------------------------------
@@ -153,6 +191,7 @@ def segmented_scan(values, seg_size: int, variant: str, engine: TileEngine,
     if variant == "grid":
         if seg_size < size:
             raise BadConfigError("the grid variant scans the whole input as one segment")
+        _check_grid_cfg(cfg)  # as grid_scan (scan.py:345-348 -> :262-265)
         if size == 0:
             raise BadLengthError("input must be a non-empty flat vector")
         if not inclusive and size % seg_size:

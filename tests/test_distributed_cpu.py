@@ -106,3 +106,30 @@ def test_shard_bounds_cover_whole_segments():
         assert spans[0][0] == 0 and spans[-1][1] == n
         for (a, b), (c, d) in zip(spans, spans[1:]):
             assert b == c and b % seg == 0
+
+
+def test_virtual_shards_match_the_process_group_path():
+    """The single-process virtual-shards mode runs the same
+    exchange arithmetic as a W-rank group: compare it with the 2-rank gloo
+    run above and with the oracle, for W = 1..8 (CPU stand-in ops)."""
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(5)
+    for n in (10_001, 4096, 77):
+        x = rng.integers(-8, 8, n).astype(np.float16)
+        xt = torch.from_numpy(x)
+        for w in (1, 2, 3, 8):
+            assert D.virtual_full_reduce(xt, w, torch.float64, ops=CpuOps).item() == x.astype(np.float64).sum()
+            for exc in (False, True):
+                got = D.virtual_full_scan(xt, w, torch.float64, exclusive=exc, ops=CpuOps).numpy()
+                assert np.array_equal(got, O.ref_seg_scan(x, n, inclusive=not exc))
+            got = D.virtual_segmented_reduce(xt, 100, w, torch.float64, ops=CpuOps).numpy()
+            assert np.array_equal(got, O.ref_seg_reduce(x, 100))
+
+
+def test_even_bounds_aligned():
+    for n, w in [(1 << 33, 8), (10_001, 3), (77, 8), (5, 4)]:
+        b = [D.even_bounds(n, w, r) for r in range(w)]
+        assert b[0][0] == 0 and b[-1][1] == n
+        for (a, c), (d, e) in zip(b, b[1:]):
+            assert c == d and c % 8 == 0 and a <= c

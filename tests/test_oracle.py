@@ -200,3 +200,66 @@ def test_bn_oracle_definition():
         vals = x[:, c].reshape(-1)
         assert m[c] == pytest.approx(vals.mean(), rel=1e-14)
         assert v[c] == pytest.approx(((vals - vals.mean()) ** 2).mean(), rel=1e-12)
+
+
+# ------------------------------------------- tolerance checkers (oracle/clib)
+
+
+def _np_bound(exact, A, dt, ulps, gamma):
+    a = np.abs(exact)
+    if dt == np.float16:
+        e = np.floor(np.log2(np.where(a > 0, a, 1.0)))
+        ulp = np.where((a > 0) & (e >= -14), 2.0 ** (e - 10), 2.0 ** -24)
+    else:
+        e = np.floor(np.log2(np.where(a > 0, a, 1.0)))
+        ulp = np.where((a > 0) & (e >= -126), 2.0 ** (e - 23), 2.0 ** -149)
+    return ulps * ulp + gamma * A
+
+
+@pytest.mark.parametrize("s", [1, 7, 64, 300, 5000, 100000])
+def test_clib_reduce_checker_matches_numpy(s):
+    from oracle import clib
+
+    rng = np.random.default_rng(s)
+    n = 50000
+    x = (rng.random(n) * 2 - 1).astype(np.float16)
+    exact = O.ref_seg_reduce(x, s)
+    A = O.ref_seg_reduce(np.abs(x), s)
+    assert np.allclose(clib.seg_reduce(x, s), exact, rtol=1e-14, atol=1e-300)
+    for dt in (np.float16, np.float32):
+        got = exact.astype(dt)
+        c = clib.check_seg_reduce(x, s, got, 1.0, 0.0)
+        assert c.bad == 0 and c.max_ratio <= 1.0, c
+        # a perturbation of 2 bounds is caught at the right place
+        bad = got.copy()
+        k = bad.size // 2
+        b = _np_bound(exact, A, dt, 1.0, 1e-6)
+        bad[k] = dt(exact[k] + 4 * b[k] + (2.0 ** -10 if dt == np.float16 else 1e-5) * abs(exact[k]))
+        c = clib.check_seg_reduce(x, s, bad, 1.0, 1e-6)
+        assert c.bad == 1 and c.first_bad == k, c
+        nan = got.copy()
+        nan[0] = np.nan
+        assert clib.check_seg_reduce(x, s, nan, 1.0, 1e-6).first_bad == 0
+
+
+@pytest.mark.parametrize("s,carry", [(16, None), (300, None), (100000, None), (100000, 2.5)])
+def test_clib_scan_checker_chunked(s, carry):
+    from oracle import clib
+
+    rng = np.random.default_rng(1)
+    n = 123457
+    x = (rng.random(n) * 2 - 1).astype(np.float16)
+    for inc in (True, False):
+        exact = O.ref_seg_scan(x, s, inc, carry)
+        got = exact.astype(np.float32)
+        ch = clib.ScanChecker(x, s, inc, carry)
+        for lo in range(0, n, 40000):
+            ch.check(lo, got[lo:lo + 40000], 1.0, 0.0)
+        assert ch.bad == 0 and ch.max_ratio <= 1.0, ch
+        if inc:
+            assert ch.exact_total == pytest.approx(exact[-1], rel=1e-13, abs=1e-13)
+        bad = got.copy()
+        bad[77777] += 1.0
+        ch = clib.ScanChecker(x, s, inc, carry)
+        ch.check(0, bad, 1.0, 1e-7)
+        assert ch.bad == 1 and ch.first_bad == 77777, ch

@@ -24,7 +24,7 @@ for p in $PARTS; do
       for cfg in "${CFGS[@]}"; do
         set -- $cfg
         timeout 600 ncu --set full --clock-control none --import-source on -k regex:seg_kernel -s 2 -c 1 \
-          -o "$OUT/prof_$1_$2_$3" -f python tests/prof_one.py $1 $2 $3 30 3 > "$OUT/prof_$1_$2_$3.log" 2>&1; echo "prof $cfg rc=$?"
+          -o "$OUT/prof_$1_$2_$3" -f python tools/prof_one.py $1 $2 $3 30 3 > "$OUT/prof_$1_$2_$3.log" 2>&1; echo "prof $cfg rc=$?"
         python tools/ncu_summary.py "$OUT/prof_$1_$2_$3.ncu-rep" > "$OUT/prof_$1_$2_$3.txt" 2>&1
         ncu -i "$OUT/prof_$1_$2_$3.ncu-rep" --page raw --csv > "$OUT/prof_$1_$2_$3.raw.csv" 2>/dev/null
         [ -n "${KEEP_REP:-}" ] || rm -f "$OUT/prof_$1_$2_$3.ncu-rep"
@@ -44,6 +44,6 @@ for p in $PARTS; do
       python tools/ncu_summary.py "$OUT/prof_bn.ncu-rep" > "$OUT/prof_bn.txt" 2>&1
       rm -f "$OUT/prof_bn.ncu-rep";;
     probe)
-      timeout 600 python tests/perf_probe.py > "$OUT/perf_probe.log" 2>&1; echo "probe rc=$?"; cat "$OUT/perf_probe.log";;
+      timeout 600 python tools/perf_probe.py > "$OUT/perf_probe.log" 2>&1; echo "probe rc=$?"; cat "$OUT/perf_probe.log";;
   esac
 done

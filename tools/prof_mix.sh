@@ -10,5 +10,5 @@ cap() {  # tag, regex, command...
   echo "== $tag"; sed -n 2,6p $OUT/$tag.txt
 }
 cap ired64 seg_kernel python tools/prof_irreg.py reduce 64 f32 3
-cap fscan16 seg_kernel python tests/prof_one.py scan 1073741824 f16 30 3
-cap gscan300 seg_kernel python tests/prof_one.py scan 300 f32 30 3
+cap fscan16 seg_kernel python tools/prof_one.py scan 1073741824 f16 30 3
+cap gscan300 seg_kernel python tools/prof_one.py scan 300 f32 30 3

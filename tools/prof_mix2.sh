@@ -8,5 +8,5 @@ cap() {
   rm -f $OUT/$tag.ncu-rep
   echo "== $tag"; sed -n 2,6p $OUT/$tag.txt; grep -A9 "stall reasons" $OUT/$tag.txt
 }
-cap red300 seg_kernel python tests/prof_one.py reduce 300 f16 30 3
-cap red2048 seg_kernel python tests/prof_one.py reduce 2048 f16 30 3
+cap red300 seg_kernel python tools/prof_one.py reduce 300 f16 30 3
+cap red2048 seg_kernel python tools/prof_one.py reduce 2048 f16 30 3

@@ -1,6 +1,6 @@
 """Run one op a few times (profiling target for ncu).
 
-usage: python tests/prof_one.py reduce|scan SEG f16|f32 [LOG2N] [REPS]
+usage: python tools/prof_one.py reduce|scan SEG f16|f32 [LOG2N] [REPS]
 """
 
 import sys

@@ -1,5 +1,5 @@
 OUT=gpurun_out/r300; mkdir -p $OUT
-ncu --set full --clock-control none --import-source on -k regex:seg_kernel -s 2 -c 1 -o $OUT/red300 -f python tests/prof_one.py reduce 300 f16 30 3 > $OUT/log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:seg_kernel -s 2 -c 1 -o $OUT/red300 -f python tools/prof_one.py reduce 300 f16 30 3 > $OUT/log 2>&1
 python tools/ncu_summary.py $OUT/red300.ncu-rep --lines 30 > $OUT/red300.txt 2>&1
 ncu -i $OUT/red300.ncu-rep --page source --csv > $OUT/red300.source.csv 2>/dev/null
 rm -f $OUT/red300.ncu-rep
