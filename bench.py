@@ -226,6 +226,39 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def hbm_read_peak(x, dev, reps=10):
+    """Measured HBM read-stream bandwidth (tools/csrc/hbm_probe.cu, a plain
+    16-byte streaming-load kernel) over the bench input: the roofline of a
+    read-only kernel.  Best of ``reps``; None if the probe is not built."""
+    import torch
+
+    so = ROOT / "tools" / "_hbm_probe.so"
+    if not so.exists():
+        return None
+    lib = ctypes.CDLL(str(so))
+    lib.hbm_read_stream.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
+                                    ctypes.c_int, ctypes.c_void_p]
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    sink = torch.zeros(sms * 4, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    nbytes = x.numel() * x.element_size()
+    best = None
+    for blocks in (sms * 2, sms * 4):
+        for _ in range(2):
+            lib.hbm_read_stream(x.data_ptr(), nbytes, sink.data_ptr(), blocks, stream.cuda_stream)
+        torch.cuda.synchronize()
+        for _ in range(reps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            lib.hbm_read_stream(x.data_ptr(), nbytes, sink.data_ptr(), blocks, stream.cuda_stream)
+            b.record(stream)
+            b.synchronize()
+            gbs = nbytes / a.elapsed_time(b) / 1e6
+            best = gbs if best is None else max(best, gbs)
+    return round(best, 1)
+
+
 def gen_device(n, device, seed):
     """Uniform [0, 1) fp16 on the device, generated in chunks."""
     import torch
@@ -336,6 +369,10 @@ def run_ours(args):
         sweep_rows.append({"seg": s, "ms": round(ms, 4), "gelem_s": round(n / ms / 1e6, 1),
                            "gbs": round(b / ms / 1e6, 1), "frac": round(b / ms / 1e6 / peak, 4)})
     achieved = tot_bytes / tot_ms / 1e6
+    read_peak = hbm_read_peak(x, dev)
+    if read_peak:
+        for r in sweep_rows:
+            r["frac_read"] = round(r["gbs"] / read_peak, 4)
     traffic = None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
@@ -343,6 +380,10 @@ def run_ours(args):
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "peak_source": peak_src,
+                "read_peak": read_peak,
+                "frac_read": round(achieved / read_peak, 4) if read_peak else None,
+                "read_peak_source": "measured in this run: tools/csrc/hbm_probe.cu 16-B "
+                                    "streaming-load kernel over the 2 GiB input, best of 20",
                 "kernel": "tc::seg_kernel<OP_REDUCE,...> (13 launches/step)",
                 "algorithmic_bytes": "2n + 2*ceil(n/s) per launch, n = 2^30"}
 
@@ -411,6 +452,9 @@ def run_ours(args):
                   "results into pinned host buffers (third stream, overlapping the next "
                   "chunks' H2D)"}
     del xh, xdev, res_h
+    e2e_per_call = None
+    if not args.no_per_call:
+        e2e_per_call = run_e2e_per_call(args, x, dev, world, barrier, max_over_ranks, outs, plans)
 
     extras = {}
     if not args.no_extras:
@@ -439,13 +483,64 @@ def run_ours(args):
             "data": "synthetic (uniform [0,1) fp16, torch.rand seeded per rank)",
             "config": config_dict(world),
             "gbs_per_gpu": round(achieved, 1),
-            "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
+            "e2e": e2e, "e2e_per_call": e2e_per_call, "gpu_launches": launches,
+            "roofline": roofline,
             "cpu_baseline": cpu, "clocks": clk.summary(), "sweep": sweep_rows,
             "extras": extras,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_e2e_per_call(args, x, dev, world, barrier, max_over_ranks, outs, plans):
+    """The drop-in exactly as a reference user calls it: a numpy fp16 array
+    in, a numpy array out, ONE public ``segmented_reduce`` call per segment
+    size -- every call copies its own 2 GiB input to the device (the
+    package's staged host path: pinned ring + host threads + copy stream) and
+    its sums back.  Host wall clock (the numpy path synchronises), max over
+    ranks; compared with the measured pinned-H2D bandwidth, the bound of a
+    call that must move its input over PCIe."""
+    import torch
+
+    import paper_1811_09736_b200 as ht
+
+    n = x.numel()
+    xn = x.cpu().numpy()
+    eng = ht.TileEngine()
+    # pinned H2D bandwidth (the per-call bound): 2 GiB pinned -> device, best of 3
+    hp = torch.empty(n, dtype=torch.float16, pin_memory=True)
+    hp.copy_(x)
+    dst = torch.empty_like(x)
+    h2d = 0.0
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dst.copy_(hp, non_blocking=True)
+        torch.cuda.synchronize()
+        h2d = max(h2d, 2 * n / (time.perf_counter() - t0) / 1e9)
+    del hp, dst
+    segs = REDUCE_SEGS
+    res = {s: ht.segmented_reduce(xn, s, plans[s], eng) for s in segs}  # warm the stager
+    barrier()
+    steps = max(1, min(args.steps, args.e2e_steps))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        res = {s: ht.segmented_reduce(xn, s, plans[s], eng) for s in segs}
+    dt = max_over_ranks(time.perf_counter() - t0) / steps
+    for s_chk in (segs[0], segs[-1]):
+        assert np.array_equal(res[s_chk], outs[s_chk].cpu().numpy()), f"per-call mismatch s={s_chk}"
+    bound = len(segs) * 2 * n / (h2d * 1e9)
+    return {"value": world * len(segs) * n / dt, "unit": UNIT, "ms_per_step": round(dt * 1e3, 2),
+            "ms_per_call": round(dt * 1e3 / len(segs), 2),
+            "h2d_bytes_per_step": len(segs) * 2 * n,
+            "d2h_bytes_per_step": sum(2 * (-(-n // s)) for s in segs),
+            "pinned_h2d_gbs": round(h2d, 1),
+            "h2d_bound_ms_per_step": round(bound * 1e3, 2),
+            "frac_of_h2d_bound": round(bound / dt, 4),
+            "api": "numpy fp16 (pageable) -> paper_1811_09736_b200.segmented_reduce(x, s, "
+                   "select_algorithm(...).variant, TileEngine()) -> numpy, one call per size, "
+                   "each call copying its own input"}
 
 
 def _time_op(fn, reps, warm, stream, barrier, max_over_ranks):
@@ -494,6 +589,30 @@ def run_extras(args, x, dev, world, rank, barrier, max_over_ranks, peak):
     out["scan_sweep_f16"] = {"workload": "segmented inclusive scan fp16, 2^30 per GPU, fp16 out",
                              "rows": rows}
     del y
+    # configs[2] with fp32 output (6 B/elem)
+    y = torch.empty(n, dtype=torch.float32, device=dev)
+    rows = []
+    for s in SCAN_SEGS:
+        ms = _time_op(lambda: D.seg_scan(x, s, torch.float32, out=y), reps, 2, stream, barrier,
+                      max_over_ranks)
+        b = 6 * n
+        rows.append({"seg": s, "ms": round(ms, 4), "gelem_s": round(world * n / ms / 1e6, 1),
+                     "gbs_per_gpu": round(b / ms / 1e6, 1), "frac": round(b / ms / 1e6 / peak, 4)})
+    out["scan_sweep_f32"] = {"workload": "segmented inclusive scan fp16, 2^30 per GPU, fp32 out",
+                             "rows": rows}
+    del y
+    # configs[1] with fp32 output
+    rows = []
+    for s in REDUCE_SEGS:
+        o = torch.empty(-(-n // s), dtype=torch.float32, device=dev)
+        ms = _time_op(lambda: D.seg_reduce(x, s, torch.float32, out=o), reps, 2, stream, barrier,
+                      max_over_ranks)
+        b = reduce_bytes(n, s, 4)
+        rows.append({"seg": s, "ms": round(ms, 4), "gelem_s": round(world * n / ms / 1e6, 1),
+                     "gbs_per_gpu": round(b / ms / 1e6, 1), "frac": round(b / ms / 1e6 / peak, 4)})
+        del o
+    out["reduce_sweep_f32"] = {"workload": "segmented reduce fp16, 2^30 per GPU, fp32 out",
+                               "rows": rows}
     # widened rows: bf16 input, non-power-of-two segment sizes
     xb = x.to(torch.bfloat16)
     rows = []
@@ -509,7 +628,7 @@ def run_extras(args, x, dev, world, rank, barrier, max_over_ranks, peak):
     del xb
     rows = []
     y = torch.empty(n, dtype=torch.float16, device=dev)
-    for s in (48, 300, 1000, 100000):
+    for s in (3, 7, 17, 48, 300, 1000, 100000):
         o = torch.empty(-(-n // s), dtype=torch.float16, device=dev)
         ms = _time_op(lambda: D.seg_reduce(x, s, torch.float16, out=o), reps, 2, stream,
                       barrier, max_over_ranks)
@@ -554,7 +673,7 @@ def run_extras(args, x, dev, world, rank, barrier, max_over_ranks, peak):
         "gbs_algorithmic": round(2 * nb / ms / 1e6, 1),
         "frac_algorithmic": round(2 * nb / ms / 1e6 / peak, 4),
         "gbs_actual": round(4 * nb / ms / 1e6, 1),
-        "passes": "tensor-core segmented reduce (mean) + centred second moment (2 reads of x)"}
+        "passes": "one read of x: per-(n, c) shifted moments + per-channel fp64 combine"}
     del xbn
     # full ops over 2^33 elements sharded across the ranks
     nf = 1 << FULL_LOG2N
@@ -605,6 +724,7 @@ def main():
                     help="approximate seconds per reference-arm step")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-per-call", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # contract: W >= 3

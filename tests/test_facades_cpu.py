@@ -9,10 +9,11 @@ import pytest
 from sklearn.base import clone
 
 import paper_1811_09736_b200 as ht
-from paper_1811_09736_b200.cli import (CSV_HEADER, _padding, emit_cost_csv, main, read_values,
+from paper_1811_09736_b200.segmented import padded_extent as _padding
+from paper_1811_09736_b200.cli import (CSV_HEADER, emit_cost_csv, main, read_values,
                                        write_values)
 from paper_1811_09736_b200.errors import BadConfigError, BadLengthError, ParseError
-from paper_1811_09736_b200.validation import as_half_batch, as_half_vector, check_positive
+from paper_1811_09736_b200.estimators import _as_batch, _positive
 from oracle import oracle as O
 
 
@@ -70,19 +71,18 @@ def test_unusable_input_exits_2(tmp_path):
 
 
 def test_validation_helpers():
-    assert as_half_vector([1, 2]).dtype == np.float16
-    with pytest.raises(BadLengthError):
-        as_half_vector([])
-    with pytest.raises(BadLengthError):
-        as_half_vector(np.ones((2, 2)))
-    with pytest.raises(BadLengthError):
-        as_half_vector(np.array(["a"]))
-    b, was_1d = as_half_batch(np.ones(8))
-    assert b.shape == (1, 8) and was_1d
-    with pytest.raises(BadLengthError):
-        as_half_batch(np.ones((2, 0)))
+    b, was_1d = _as_batch([1, 2])
+    assert b.dtype == np.float16 and b.shape == (1, 2) and was_1d
+    for bad in ([], np.ones((2, 0)), np.ones((2, 2, 2)), np.array(["a"])):
+        with pytest.raises(BadLengthError):
+            _as_batch(bad)
+    b, was_1d = _as_batch(np.ones((3, 8)))
+    assert b.shape == (3, 8) and not was_1d
     with pytest.raises(BadConfigError):
-        check_positive("wpb", 0)
+        _positive("wpb", 0)
+    with pytest.raises(BadConfigError):
+        _positive("wpb", 2.0)
+    assert _positive("wpb", np.int64(3)) == 3
 
 
 def test_estimator_protocol(rng):
