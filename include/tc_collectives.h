@@ -163,6 +163,16 @@ int tc_irreg_scan(const void* x, int in_dtype, int64_t n, const int64_t* offsets
 int tc_bn_stats(const void* x, int in_dtype, int64_t N, int64_t C, int64_t HW, void* mean,
                 void* var, int out_dtype, void* ws, size_t ws_bytes, void* stream);
 
+/* Diagnostics: which kernel a tc_seg_reduce / tc_seg_scan call with these
+ * arguments runs.  *mode: 0 LOCAL, 1 ROWS, 2 TILES, 3 GENERAL, 4 CHUNK,
+ * 5 IRREG, 6 GSCR, 7 ROWSEG (whole segments per TMA row).  *row_len: the
+ * elements of one MMA row -- 64, or k * seg for ROWSEG (rows of k whole
+ * segments).  A non-finite input poisons the outputs computed from its MMA
+ * row accumulation: the 64-element row, the whole ROWSEG row for a reduce,
+ * the 64-column chunk of the ROWSEG row for a scan. */
+int tc_plan_info(int op, int64_t n, int64_t seg, int out_dtype, int has_carry, int has_total,
+                 int* mode, int64_t* row_len);
+
 /* Human-readable name of a status code. */
 const char* tc_status_string(int status);
 
@@ -175,7 +185,7 @@ uint64_t tc_launch_count(void);
 void tc_reset_launch_count(void);
 
 /* ABI version: (major << 16) | minor.  1.1 added the *_ex entry points,
- * 1.2 the tc_irreg_* entry points, 1.3 tc_bn_stats. */
+ * 1.2 the tc_irreg_* entry points, 1.3 tc_bn_stats, 1.4 tc_plan_info. */
 int tc_abi_version(void);
 
 #ifdef __cplusplus

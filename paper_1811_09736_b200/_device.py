@@ -214,3 +214,20 @@ def bn_stats(x: torch.Tensor, out_dtype=torch.float32):
                                 var.data_ptr(), _DT[out_dtype], ws.data_ptr(), ws.numel(),
                                 _stream_ptr(x.device)))
     return mean, var
+
+
+MODES = ("LOCAL", "ROWS", "TILES", "GENERAL", "CHUNK", "IRREG", "GSCR", "ROWSEG")
+
+
+def plan_info(op: str, n: int, seg: int, out_dtype=torch.float16, carry_in: bool = False,
+              total_out: bool = False) -> tuple[str, int]:
+    """(kernel mode, MMA row length in elements) a seg_reduce / seg_scan
+    call would use (tc_plan_info; host-only, no device work)."""
+    import ctypes
+
+    mode = ctypes.c_int(0)
+    row = ctypes.c_int64(0)
+    _check(_lib.lib.tc_plan_info(_lib.TC_OP_REDUCE if op == "reduce" else _lib.TC_OP_SCAN, n, seg,
+                                 _DT[out_dtype], int(carry_in), int(total_out),
+                                 ctypes.byref(mode), ctypes.byref(row)))
+    return MODES[mode.value], int(row.value)

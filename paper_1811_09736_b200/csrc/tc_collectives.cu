@@ -94,6 +94,7 @@ constexpr int MODE_TILES = 2;
 constexpr int MODE_GENERAL = 3;
 constexpr int MODE_CHUNK = 4;
 constexpr int MODE_IRREG = 5;  // irregular segments from a CSR offsets array
+constexpr int MODE_ROWSEG = 7;  // whole segments per TMA row (rowseg_*_kernel)
 constexpr int MODE_GSCR = 6;   // GENERAL reduce with many segment ends per row (2m < GR):
                                // end values staged in SMEM, interior segments stored coalesced
 constexpr int kMaxCtas = 1024;                    // persistent grid cap
@@ -681,6 +682,7 @@ __global__ void __launch_bounds__(kTailThreads) irreg_tail_kernel(const __half* 
 // produce, so this consumer runs on CUDA cores; the mean alone is the
 // tensor-core segmented reduce (tc_seg_reduce_ex, s = HW).
 constexpr int kBnThreads = 256;
+constexpr long long kBnWarpMin = 2048;  // segments this long get a warp each
 
 __device__ __forceinline__ double block_sum_d(double v, double* sred) {
   v = warp_sum_d(v);
@@ -739,6 +741,60 @@ __global__ void __launch_bounds__(kBnThreads) bn_moments_kernel(const __half* x,
       if (lane == 0) mom[q] = make_double2(d1, d2);
     }
   };
+  // small segments (HW < kBnWarpMin): one THREAD per (n, c) segment -- a
+  // warp reads 32 neighbouring segments, so every sector it touches is used
+  // within a few iterations (L1), and the per-segment sums need no shuffles
+  auto run_thread = [&](auto vec_tag) {
+    constexpr int V = decltype(vec_tag)::value;
+    using VT = typename std::conditional<V == 8, uint4,
+               typename std::conditional<V == 4, uint2,
+               typename std::conditional<V == 2, uint32_t, unsigned short>::type>::type>::type;
+    const long long nv = HW / V;
+    for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q < nsegs;
+         q += static_cast<long long>(gridDim.x) * blockDim.x) {
+      const long long c = q % C;
+      const float k = in_to_float(x, c * HW, bf16);
+      // four interleaved accumulators (one per load in flight): shorter
+      // fp32 chains, both for latency and for rounding error
+      float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+      auto acc = [&](const VT& w, int u) {
+        const unsigned short* h = reinterpret_cast<const unsigned short*>(&w);
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          const float f = bf16 ? __uint_as_float(static_cast<uint32_t>(h[e]) << 16)
+                               : __half2float(__ushort_as_half(h[e]));
+          const float a = f - k;
+          s1[u] += a;
+          s2[u] = fmaf(a, a, s2[u]);
+        }
+      };
+      const VT* xv = reinterpret_cast<const VT*>(x + q * HW);
+      long long i = 0;
+      for (; i + 3 < nv; i += 4) {
+        const VT a = __ldg(xv + i), b = __ldg(xv + i + 1), cc = __ldg(xv + i + 2),
+                 d = __ldg(xv + i + 3);
+        acc(a, 0);
+        acc(b, 1);
+        acc(cc, 2);
+        acc(d, 3);
+      }
+      for (; i < nv; ++i) acc(__ldg(xv + i), 0);
+      mom[q] = make_double2(
+          (static_cast<double>(s1[0]) + s1[1]) + (static_cast<double>(s1[2]) + s1[3]),
+          (static_cast<double>(s2[0]) + s2[1]) + (static_cast<double>(s2[2]) + s2[3]));
+    }
+  };
+  if (HW < kBnWarpMin) {
+    if ((HW & 7) == 0)
+      run_thread(std::integral_constant<int, 8>{});
+    else if ((HW & 3) == 0)
+      run_thread(std::integral_constant<int, 4>{});
+    else if ((HW & 1) == 0)
+      run_thread(std::integral_constant<int, 2>{});
+    else
+      run_thread(std::integral_constant<int, 1>{});
+    return;
+  }
   if ((HW & 7) == 0)
     run(std::integral_constant<int, 8>{});
   else if ((HW & 3) == 0)
@@ -749,19 +805,83 @@ __global__ void __launch_bounds__(kBnThreads) bn_moments_kernel(const __half* x,
     run(std::integral_constant<int, 1>{});
 }
 
+// Long, 16-byte aligned segments (HW % 8 == 0, HW >= kBnChanMin): block
+// (c, sp) streams channel c of samples [n0, n1) -- a flat index over the
+// 8-element vectors of those segments, four 16-byte loads in flight per
+// thread -- and accumulates ONE (S1, S2) pair for the channel (every element
+// shares K_c), so the scratch is [splits][C] instead of [N][C].
+constexpr long long kBnChanMin = 512;
+
+__global__ void __launch_bounds__(kBnThreads) bn_chan_kernel(const __half* x, int in_bf16,
+                                                             long long N, long long C,
+                                                             long long HW, double2* mom) {
+  __shared__ double sred[kBnThreads / 32];
+  const long long c = blockIdx.x;
+  const int splits = gridDim.y, sp = blockIdx.y;
+  const long long n0 = N * sp / splits, n1 = N * (sp + 1) / splits;
+  const bool bf16 = in_bf16 != 0;
+  const float k = in_to_float(x, c * HW, bf16);
+  const long long nv = HW / 8;                  // vectors per segment
+  const long long total = (n1 - n0) * nv;
+  const uint4* base = reinterpret_cast<const uint4*>(x);
+  auto addr = [&](long long i) -> long long {  // vector index in x of flat vector i
+    const long long q = i / nv;
+    return ((n0 + q) * C + c) * nv + (i - q * nv);
+  };
+  float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+  auto acc = [&](const uint4& w, int u) {
+    const unsigned short* h = reinterpret_cast<const unsigned short*>(&w);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float f = bf16 ? __uint_as_float(static_cast<uint32_t>(h[e]) << 16)
+                           : __half2float(__ushort_as_half(h[e]));
+      const float a = f - k;
+      s1[u] += a;
+      s2[u] = fmaf(a, a, s2[u]);
+    }
+  };
+  double d1 = 0.0, d2 = 0.0;
+  const long long step = blockDim.x;
+  long long i = threadIdx.x;
+  int it = 0;
+  for (; i + 3 * step < total; i += 4 * step) {
+    const uint4 a = __ldcs(base + addr(i)), b = __ldcs(base + addr(i + step)),
+                cc = __ldcs(base + addr(i + 2 * step)), d = __ldcs(base + addr(i + 3 * step));
+    acc(a, 0);
+    acc(b, 1);
+    acc(cc, 2);
+    acc(d, 3);
+    if (++it == 16) {  // flush the fp32 partials to fp64 every 512 elements per slot
+      d1 += (static_cast<double>(s1[0]) + s1[1]) + (static_cast<double>(s1[2]) + s1[3]);
+      d2 += (static_cast<double>(s2[0]) + s2[1]) + (static_cast<double>(s2[2]) + s2[3]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s1[u] = s2[u] = 0.f;
+      it = 0;
+    }
+  }
+  for (; i < total; i += step) acc(__ldcs(base + addr(i)), 0);
+  d1 += (static_cast<double>(s1[0]) + s1[1]) + (static_cast<double>(s1[2]) + s1[3]);
+  d2 += (static_cast<double>(s2[0]) + s2[1]) + (static_cast<double>(s2[2]) + s2[3]);
+  const double t1 = block_sum_d(d1, sred);
+  const double t2 = block_sum_d(d2, sred);
+  if (threadIdx.x == 0) mom[static_cast<long long>(sp) * C + c] = make_double2(t1, t2);
+}
+
 template <typename OutT>
 __global__ void __launch_bounds__(kBnThreads) bn_finish_kernel(const __half* x, int in_bf16,
                                                                long long N, long long C,
                                                                long long HW, double2* mom,
-                                                               OutT* mean_out, OutT* var_out) {
+                                                               long long groups, OutT* mean_out,
+                                                               OutT* var_out) {
   __shared__ double sred[kBnThreads / 32];
   const long long c = blockIdx.x;
   double a1 = 0.0, a2 = 0.0;
-  for (long long n = threadIdx.x; n < N; n += blockDim.x) {
-    const double2 m = mom[n * C + c];
+  // mom[g * C + c], g < groups: per (n, c) segment or per (split, c) block
+  for (long long g = threadIdx.x; g < groups; g += blockDim.x) {
+    const double2 m = mom[g * C + c];
     a1 += m.x;
     a2 += m.y;
-    mom[n * C + c] = make_double2(0.0, 0.0);  // leave the workspace zeroed
+    mom[g * C + c] = make_double2(0.0, 0.0);  // leave the workspace zeroed
   }
   const double s1 = block_sum_d(a1, sred);
   const double s2 = block_sum_d(a2, sred);
@@ -1503,7 +1623,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
             float run = 0.f, head = 0.f;
             int seen = 0;
             if constexpr (MODE == MODE_GSCR) {
-              if (et == 0) misc->tile_o[par] = qdiv;  // first segment ending in this tile
+              if (rit == 0) misc->tile_o[par] = qdiv;  // first segment ending in this tile (row 0)
             }
             if (dl >= GR && row != p.rows_full) {
               // a full row that does not hold the input's last granule
@@ -1529,19 +1649,31 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
                 seen = 1;
               } else if (p.m >= GR) {
                 // at most one end (granule e0; GR = none): head = granules
-                // 0..e0, the open tail = the rest
+                // 0..e0, the open tail = the rest.  Eight interleaved
+                // accumulators per piece (short dependency chains: the sums
+                // are latency-, not issue-bound), then a fixed tree.
                 const int e0 = rem0 < GR ? static_cast<int>(rem0) : GR;
-                float a = 0.f, b = 0.f;
+                constexpr int NA = GR < 8 ? GR : 8;
+                float ha[NA], ta[NA];
+  #pragma unroll
+                for (int q = 0; q < NA; ++q) ha[q] = ta[q] = 0.f;
   #pragma unroll
                 for (int j = 0; j < GR; ++j) {
                   if (j <= e0)
-                    a += gs[j];
+                    ha[j % NA] += gs[j];
                   else
-                    b += gs[j];
+                    ta[j % NA] += gs[j];
                 }
+  #pragma unroll
+                for (int w = NA / 2; w >= 1; w >>= 1)
+  #pragma unroll
+                  for (int q = 0; q < w; ++q) {
+                    ha[q] += ha[q + w];
+                    ta[q] += ta[q + w];
+                  }
                 seen = e0 < GR;
-                head = a;
-                run = seen ? b : a;
+                head = ha[0];
+                run = seen ? ta[0] : ha[0];
               } else {
                 // at most two ends (2m >= GR): head, one interior segment, tail
                 const int e0 = rem0 < GR ? static_cast<int>(rem0) : GR;
@@ -2169,6 +2301,512 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
 }
 
 // =====================================================================
+// MODE_ROWSEG reduce: whole segments per TMA row.
+//
+// For a segment size s with few factors of two (g = gcd(s, 64) <= 8, i.e.
+// 8 or more granules per 64-element row), the granule formulation leaves
+// many segment ends inside every row and a per-element walk in the
+// epilogue.  Instead the input is viewed as a matrix X[R x L] whose rows
+// hold k WHOLE segments, L = k s with 2L a multiple of 16 bytes (k a
+// multiple of 8 / gcd(s, 8)) -- the paper's strided Reduction16n, where
+// column c of the loaded tile is segment c, with the stride chosen so TMA
+// can walk it.  A row is ceil(L / 64) SW128 chunks of 64 columns (TMA
+// zero-fills the columns past L); the MMA accumulates every chunk c of a
+// 128-row block against its own indicator B_c[k'][j] = [(64c + k') / s ==
+// j] into one TMEM accumulator, so column j of row r is exactly the sum of
+// segment r k + j, computed from that segment's elements only.  No segment
+// crosses a row, so there is no carry chain and no cross-CTA fixup: the
+// epilogue stores k consecutive outputs per row.  The tail of n - R L < L
+// elements (< k + 1 segments, the last possibly ragged) is summed in fp64
+// by the last CTA.
+constexpr int kRsStages = 4;
+constexpr int kRsAcc = 4;
+constexpr uint32_t kRsMaxB = 24 * 1024;  // B matrices (ring 64 KB + B + staging 16 KB: 2 CTAs / SM)
+constexpr int kRsMaxRowBytes = 64;       // k * sizeof(out) <= 64: one staging buffer <= 8 KB
+
+struct RsParams {
+  const __half* x;
+  int in_bf16;
+  void* out;
+  long long n, s, L, R, nblk;  // elements, segment, row length, rows, 128-row blocks
+  int k, nchunk;               // segments per row, 64-column chunks per row
+};
+
+struct RsMisc {
+  uint64_t full[kRsStages];
+  uint64_t empty[kRsStages];
+  uint64_t tfull[kRsAcc];
+  uint64_t tempty[kRsAcc];
+  uint32_t tmem_base;
+};
+
+__host__ __device__ constexpr int rs_n(int ks) { return ks < 16 ? 16 : ks; }  // UMMA N (a multiple of 16)
+constexpr uint32_t kRsOffB = kRsStages * kTileBytes;
+// dynamic shared memory of a launch: ring + nchunk B matrices + 2 output
+// staging buffers (128 rows x row_bytes) + misc
+__host__ __device__ inline uint32_t rs_off_stg(int nch, int n) {
+  return kRsOffB + ((static_cast<uint32_t>(nch) * n * 128 + 1023) / 1024) * 1024;
+}
+__host__ __device__ inline uint32_t rs_off_misc(int nch, int n, int row_bytes) {
+  return rs_off_stg(nch, n) + 2 * kTileRows * static_cast<uint32_t>(row_bytes);
+}
+constexpr uint32_t kRsSmemMax =
+    kRsOffB + kRsMaxB + 2 * kTileRows * kRsMaxRowBytes + sizeof(RsMisc) + 2048;
+
+template <typename OutT, int KS>
+__global__ void __launch_bounds__(kThreads, 2)
+    rowseg_reduce_kernel(const __grid_constant__ CUtensorMap tin,
+                         const __grid_constant__ CUtensorMap tout, const RsParams p) {
+  constexpr int kRsN = rs_n(KS);
+  constexpr uint32_t kRsBBytes = kRsN * 128;  // one chunk's B: N rows of 128 B
+  // rows of >= 16 output bytes go through SMEM and one TMA store per block
+  // (a contiguous 128 * KS-output region): direct per-lane stores would
+  // scatter 16-byte pieces over 32 lines per instruction
+  constexpr int kRowBytes = KS * static_cast<int>(sizeof(OutT));
+  constexpr bool kStage = kRowBytes >= 16;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  RsMisc* misc =
+      reinterpret_cast<RsMisc*>(smem + rs_off_misc(p.nchunk, kRsN, kStage ? kRowBytes : 0));
+  uint8_t* stg_base = smem + rs_off_stg(p.nchunk, kRsN);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long b_begin = p.nblk * blockIdx.x / gridDim.x;
+  const long long b_end = p.nblk * (blockIdx.x + 1) / gridDim.x;
+  const int nch = p.nchunk;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tin);
+    if (kStage) ptx::prefetch_tmap(&tout);
+    for (int i = 0; i < kRsStages; ++i) {
+      ptx::mbar_init(&misc->full[i], 1);
+      ptx::mbar_init(&misc->empty[i], 1);
+    }
+    for (int a = 0; a < kRsAcc; ++a) {
+      ptx::mbar_init(&misc->tfull[a], 1);
+      ptx::mbar_init(&misc->tempty[a], kEpiThreads);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc(&misc->tmem_base, kRsAcc * kRsN < 32 ? 32 : kRsAcc * kRsN);
+    ptx::tmem_relinquish();
+  }
+  // the per-chunk indicator matrices, K-major, 128-B swizzled (row j = B[.][j])
+  const uint16_t one = p.in_bf16 ? 0x3F80 : 0x3C00;
+  for (int idx = threadIdx.x; idx < nch * kRsN * 8; idx += blockDim.x) {
+    const int c = idx / (kRsN * 8), rem = idx % (kRsN * 8);
+    const int j = rem >> 3, pos = rem & 7;
+    const int lc = pos ^ (j & 7);
+    __align__(16) uint16_t h[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const long long col = 64LL * c + lc * 8 + e;  // column of the row
+      h[e] = (j < p.k && col < p.L && col / p.s == j) ? one : 0;
+    }
+    *reinterpret_cast<uint4*>(smem + kRsOffB + c * kRsBBytes + j * 128 + pos * 16) =
+        *reinterpret_cast<uint4*>(h);
+  }
+  ptx::fence_proxy_async_smem();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = misc->tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = ptx::policy_evict_first();
+      int i = 0;
+      for (long long b = b_begin; b < b_end; ++b)
+        for (int c = 0; c < nch; ++c, ++i) {
+          const int st = i % kRsStages;
+          ptx::mbar_wait(&misc->empty[st], ((i / kRsStages) & 1) ^ 1u);
+          ptx::mbar_arrive_expect_tx(&misc->full[st], kTileBytes);
+          ptx::tma_load_2d(&tin, smem + st * kTileBytes, &misc->full[st], 64 * c,
+                           static_cast<int32_t>(b * kTileRows), pol);
+        }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc =
+          ptx::idesc_f16_f32(128, kRsN) | (p.in_bf16 ? ((1u << 7) | (1u << 10)) : 0u);
+      int i = 0, blk = 0;
+      for (long long b = b_begin; b < b_end; ++b, ++blk) {
+        const int a = blk % kRsAcc;
+        ptx::mbar_wait(&misc->tempty[a], ((blk / kRsAcc) & 1) ^ 1u);
+        for (int c = 0; c < nch; ++c, ++i) {
+          const int st = i % kRsStages;
+          ptx::mbar_wait(&misc->full[st], (i / kRsStages) & 1);
+          ptx::tc_fence_after();
+          const uint64_t adesc = ptx::smem_desc_sw128(smem + st * kTileBytes);
+          const uint64_t bdesc = ptx::smem_desc_sw128(smem + kRsOffB + c * kRsBBytes);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            ptx::mma_f16_ss(tmem + a * kRsN, adesc + 2 * kk, bdesc + 2 * kk, idesc,
+                            (c > 0 || kk > 0) ? 1u : 0u);
+          ptx::mma_commit(&misc->empty[st]);
+        }
+        ptx::mma_commit(&misc->tfull[a]);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int qd = warp & 3;
+    const int rit = qd * 32 + lane;
+    const int et = threadIdx.x - 64;
+    const uint32_t lane_base = static_cast<uint32_t>(qd * 32) << 16;
+    OutT* out = reinterpret_cast<OutT*>(p.out);
+    int blk = 0;
+    for (long long b = b_begin; b < b_end; ++b, ++blk) {
+      const int a = blk % kRsAcc;
+      ptx::mbar_wait_warp(&misc->tfull[a], (blk / kRsAcc) & 1);
+      ptx::tc_fence_after();
+      uint32_t r[KS];
+      if constexpr (KS <= 32) {
+        ptx::tmem_ld_32x32b<KS>(tmem + lane_base + a * kRsN, r);
+      } else {
+        uint32_t(&r0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[0]);
+        uint32_t(&r1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[32]);
+        ptx::tmem_ld_32x32b<32>(tmem + lane_base + a * kRsN, r0);
+        ptx::tmem_ld_32x32b<32>(tmem + lane_base + a * kRsN + 32, r1);
+      }
+      ptx::tmem_wait_ld();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&misc->tempty[a]);
+      const long long row = b * kTileRows + rit;
+      float v[KS];
+#pragma unroll
+      for (int j = 0; j < KS; ++j) v[j] = __uint_as_float(r[j]) + 0.f;  // -0 -> +0
+      if constexpr (kStage) {
+        uint8_t* stg = stg_base + (blk & 1) * (kTileRows * kRowBytes);
+        if (et == 0) ptx::bulk_wait_read<1>();  // the store that used this buffer has read it
+        ptx::named_bar_sync(kEpiBar, kEpiThreads);
+        uint8_t* dst = stg + rit * kRowBytes;
+        if constexpr (sizeof(OutT) == 2) {
+#pragma unroll
+          for (int q = 0; q < KS / 8; ++q) {
+            uint4 w;
+            __half2 h0 = __floats2half2_rn(v[8 * q + 0], v[8 * q + 1]);
+            __half2 h1 = __floats2half2_rn(v[8 * q + 2], v[8 * q + 3]);
+            __half2 h2 = __floats2half2_rn(v[8 * q + 4], v[8 * q + 5]);
+            __half2 h3 = __floats2half2_rn(v[8 * q + 6], v[8 * q + 7]);
+            w.x = *reinterpret_cast<uint32_t*>(&h0);
+            w.y = *reinterpret_cast<uint32_t*>(&h1);
+            w.z = *reinterpret_cast<uint32_t*>(&h2);
+            w.w = *reinterpret_cast<uint32_t*>(&h3);
+            reinterpret_cast<uint4*>(dst)[q] = w;
+          }
+        } else if constexpr (sizeof(OutT) == 4) {
+#pragma unroll
+          for (int q = 0; q < KS / 4; ++q)
+            reinterpret_cast<float4*>(dst)[q] =
+                make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < KS / 2; ++q)
+            reinterpret_cast<double2*>(dst)[q] =
+                make_double2(static_cast<double>(v[2 * q]), static_cast<double>(v[2 * q + 1]));
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(kEpiBar, kEpiThreads);
+        if (et == 0) {
+          ptx::tma_store_2d(&tout, stg, 0, static_cast<int32_t>(b * kTileRows));
+          ptx::bulk_commit();
+        }
+      } else if (row < p.R) {
+        store_run<OutT, KS>(out, row * KS, v, row * KS + KS - 1);
+      }
+    }
+    if (kStage && et == 0) ptx::bulk_wait<0>();
+    // the tail past R rows: < k + 1 segments, summed in fp64 by the last CTA
+    if (blockIdx.x == gridDim.x - 1) {
+      const long long base = p.R * p.L;
+      const long long ntail = (p.n - base + p.s - 1) / p.s;
+      for (long long j = et; j < ntail; j += kEpiThreads) {
+        const long long lo = base + j * p.s;
+        const long long hi = lo + p.s < p.n ? lo + p.s : p.n;
+        double acc = 0.0;
+        for (long long e = lo; e < hi; ++e) acc += in_to_float(p.x, e, p.in_bf16 != 0);
+        out[p.R * KS + j] = cvt_out_d<OutT>(acc + 0.0);
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, kRsAcc * kRsN < 32 ? 32 : kRsAcc * kRsN);
+  }
+}
+
+// =====================================================================
+// MODE_ROWSEG scan: the same whole-segments-per-row view for the scan.
+//
+// X[R x L], L = k s, k whole segments per row, ceil(L / 64) chunks per row.
+// Chunk c of a 128-row block is multiplied by U_c[k'][j] = [seg(64c + k')
+// == seg(64c + j) and k' <= j] (the block-diagonal upper-triangular ones of
+// the paper's A.U row scan, with blocks = the segment pieces inside the
+// chunk), so TMEM holds the inclusive in-segment prefix of every piece.  A
+// segment that started in an earlier chunk of the same row continues with
+// that chunk's last inclusive value (one carry per thread, added to the
+// leading columns below the chunk's first segment start -- a position
+// shared by every row).  Exclusive outputs are the inclusive ones shifted
+// by one column inside each segment.  No segment crosses a row: no
+// carries between rows, tiles or CTAs.  Outputs go through swizzled SMEM
+// staging and TMA bulk-tensor stores into the same [R x L] view; the tail
+// of n - R L < L elements is scanned in fp64 by the last CTA.
+constexpr int kRssStages = 4;
+constexpr int kRssAcc = 8;  // 8 x 64 TMEM columns: 1 CTA / SM
+constexpr int kRssMaxChunks = 10;
+constexpr uint32_t kRssOffB = kRssStages * kTileBytes;
+constexpr uint32_t kRssOffOut = kRssOffB + kRssMaxChunks * 8192;
+
+struct RssMisc {
+  uint64_t full[kRssStages];
+  uint64_t empty[kRssStages];
+  uint64_t tfull[kRssAcc];
+  uint64_t tempty[kRssAcc];
+  uint64_t smask[kRssMaxChunks];  // segment starts in chunk c (bit j = column 64c + j)
+  int fs[kRssMaxChunks];          // first start column in chunk c (64: none)
+  int cont[kRssMaxChunks];        // chunk c's last segment continues into chunk c + 1
+  uint32_t tmem_base;
+};
+
+template <typename OutT>
+constexpr uint32_t rss_smem() {
+  return kRssOffOut + 2 * kTileElems * sizeof(OutT) + sizeof(RssMisc) + 1024;
+}
+
+struct RssParams {
+  const __half* x;
+  int in_bf16;
+  void* out;
+  long long n, s, L, R, nblk;
+  int nchunk, exclusive;
+};
+
+template <typename OutT>
+__global__ void __launch_bounds__(kThreads, 1)
+    rowseg_scan_kernel(const __grid_constant__ CUtensorMap tin,
+                       const __grid_constant__ CUtensorMap tout, const RssParams p) {
+  constexpr uint32_t kOutBytes = kTileElems * sizeof(OutT);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  RssMisc* misc = reinterpret_cast<RssMisc*>(smem + kRssOffOut + 2 * kOutBytes);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long b_begin = p.nblk * blockIdx.x / gridDim.x;
+  const long long b_end = p.nblk * (blockIdx.x + 1) / gridDim.x;
+  const int nch = p.nchunk;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tin);
+    ptx::prefetch_tmap(&tout);
+    for (int i = 0; i < kRssStages; ++i) {
+      ptx::mbar_init(&misc->full[i], 1);
+      ptx::mbar_init(&misc->empty[i], 1);
+    }
+    for (int a = 0; a < kRssAcc; ++a) {
+      ptx::mbar_init(&misc->tfull[a], 1);
+      ptx::mbar_init(&misc->tempty[a], kEpiThreads);
+    }
+    // the chunk geometry is the same for every row
+    for (int c = 0; c < nch; ++c) {
+      const long long c0 = 64LL * c;
+      const long long first = ((c0 + p.s - 1) / p.s) * p.s;
+      uint64_t m = 0;
+      for (long long q = first; q < c0 + 64 && q < p.L; q += p.s) m |= 1ull << (q - c0);
+      misc->smask[c] = m;
+      misc->fs[c] = first - c0 < 64 ? static_cast<int>(first - c0) : 64;
+      misc->cont[c] = (c + 1 < nch) && ((c0 + 64) % p.s != 0);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc(&misc->tmem_base, kRssAcc * 64);
+    ptx::tmem_relinquish();
+  }
+  // U_c, K-major, 128-B swizzled: row j (output column) holds U_c[k'][j]
+  const uint16_t one = p.in_bf16 ? 0x3F80 : 0x3C00;
+  for (int idx = threadIdx.x; idx < nch * 64 * 8; idx += blockDim.x) {
+    const int c = idx >> 9, rem = idx & 511;
+    const int j = rem >> 3, pos = rem & 7;
+    const int lc = pos ^ (j & 7);
+    const long long cj = 64LL * c + j;
+    __align__(16) uint16_t h[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int kk = lc * 8 + e;
+      const long long ck = 64LL * c + kk;
+      h[e] = (ck < p.L && cj < p.L && kk <= j && ck / p.s == cj / p.s) ? one : 0;
+    }
+    *reinterpret_cast<uint4*>(smem + kRssOffB + c * 8192 + j * 128 + pos * 16) =
+        *reinterpret_cast<uint4*>(h);
+  }
+  ptx::fence_proxy_async_smem();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = misc->tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = ptx::policy_evict_first();
+      int i = 0;
+      for (long long b = b_begin; b < b_end; ++b)
+        for (int c = 0; c < nch; ++c, ++i) {
+          const int st = i % kRssStages;
+          ptx::mbar_wait(&misc->empty[st], ((i / kRssStages) & 1) ^ 1u);
+          ptx::mbar_arrive_expect_tx(&misc->full[st], kTileBytes);
+          ptx::tma_load_2d(&tin, smem + st * kTileBytes, &misc->full[st], 64 * c,
+                           static_cast<int32_t>(b * kTileRows), pol);
+        }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc =
+          ptx::idesc_f16_f32(128, 64) | (p.in_bf16 ? ((1u << 7) | (1u << 10)) : 0u);
+      int i = 0;
+      for (long long b = b_begin; b < b_end; ++b)
+        for (int c = 0; c < nch; ++c, ++i) {
+          const int st = i % kRssStages;
+          const int a = i % kRssAcc;
+          ptx::mbar_wait(&misc->tempty[a], ((i / kRssAcc) & 1) ^ 1u);
+          ptx::mbar_wait(&misc->full[st], (i / kRssStages) & 1);
+          ptx::tc_fence_after();
+          const uint64_t adesc = ptx::smem_desc_sw128(smem + st * kTileBytes);
+          const uint64_t bdesc = ptx::smem_desc_sw128(smem + kRssOffB + c * 8192);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            ptx::mma_f16_ss(tmem + a * 64, adesc + 2 * kk, bdesc + 2 * kk, idesc,
+                            kk > 0 ? 1u : 0u);
+          ptx::mma_commit(&misc->empty[st]);
+          ptx::mma_commit(&misc->tfull[a]);
+        }
+    }
+    __syncwarp();
+  } else {
+    const int qd = warp & 3;
+    const int rit = qd * 32 + lane;
+    const int et = threadIdx.x - 64;
+    const bool leader = (et == 0);
+    const uint32_t lane_base = static_cast<uint32_t>(qd * 32) << 16;
+    const bool excl = p.exclusive != 0;
+    int i = 0;
+    for (long long b = b_begin; b < b_end; ++b) {
+      float carry = 0.f;  // inclusive value of the segment continuing into chunk c
+      for (int c = 0; c < nch; ++c, ++i) {
+        const int a = i % kRssAcc;
+        const int par = i & 1;
+        ptx::mbar_wait_warp(&misc->tfull[a], (i / kRssAcc) & 1);
+        ptx::tc_fence_after();
+        uint32_t r[64];
+        {
+          uint32_t(&r0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[0]);
+          uint32_t(&r1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[32]);
+          ptx::tmem_ld_32x32b<32>(tmem + lane_base + a * 64, r0);
+          ptx::tmem_ld_32x32b<32>(tmem + lane_base + a * 64 + 32, r1);
+        }
+        ptx::tmem_wait_ld();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&misc->tempty[a]);
+        // uniform chunk geometry: the first segment start at or after column
+        // 64c (fs, 64 = none in this chunk), segment starts as a bit mask,
+        // and whether the chunk's last segment continues into chunk c + 1
+        const long long c0 = 64LL * c;
+        const int fs = misc->fs[c];
+        const uint64_t smask = misc->smask[c];
+        const bool cont = misc->cont[c] != 0;
+        float v[64];
+#pragma unroll
+        for (int j = 0; j < 64; ++j) v[j] = __uint_as_float(r[j]) + (j < fs ? carry : 0.f);
+        const float last = v[63];
+        if (excl) {
+          const uint32_t mlo = static_cast<uint32_t>(smask), mhi = static_cast<uint32_t>(smask >> 32);
+#pragma unroll
+          for (int j = 63; j >= 0; --j) {
+            const bool st = ((j < 32 ? mlo : mhi) >> (j & 31)) & 1u;
+            v[j] = st ? 0.f : (j ? v[j - 1] : carry);
+          }
+        }
+        carry = cont ? last : 0.f;
+        // stage (swizzled, as the output tensor map's SW128 box) and store
+        if (leader) ptx::bulk_wait_read<1>();
+        ptx::named_bar_sync(kEpiBar, kEpiThreads);
+        uint8_t* stg = smem + kRssOffOut + par * kOutBytes;
+        const uint32_t rb = static_cast<uint32_t>(rit) * 128u;
+        const uint32_t sw = static_cast<uint32_t>(rit & 7);
+        if constexpr (sizeof(OutT) == 2) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            uint4 w;
+            __half2 h0 = __floats2half2_rn(v[8 * q + 0] + 0.f, v[8 * q + 1] + 0.f);
+            __half2 h1 = __floats2half2_rn(v[8 * q + 2] + 0.f, v[8 * q + 3] + 0.f);
+            __half2 h2 = __floats2half2_rn(v[8 * q + 4] + 0.f, v[8 * q + 5] + 0.f);
+            __half2 h3 = __floats2half2_rn(v[8 * q + 6] + 0.f, v[8 * q + 7] + 0.f);
+            w.x = *reinterpret_cast<uint32_t*>(&h0);
+            w.y = *reinterpret_cast<uint32_t*>(&h1);
+            w.z = *reinterpret_cast<uint32_t*>(&h2);
+            w.w = *reinterpret_cast<uint32_t*>(&h3);
+            *reinterpret_cast<uint4*>(stg + rb + ((q ^ sw) << 4)) = w;
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float4 w = make_float4(v[32 * h + 4 * q] + 0.f, v[32 * h + 4 * q + 1] + 0.f,
+                                     v[32 * h + 4 * q + 2] + 0.f, v[32 * h + 4 * q + 3] + 0.f);
+              *reinterpret_cast<float4*>(stg + h * 16384 + rb + ((q ^ sw) << 4)) = w;
+            }
+          }
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(kEpiBar, kEpiThreads);
+        if (leader) {
+          const int32_t r0 = static_cast<int32_t>(b * kTileRows);
+          if constexpr (sizeof(OutT) == 2) {
+            ptx::tma_store_2d(&tout, stg, static_cast<int32_t>(c0), r0);
+          } else {
+            ptx::tma_store_2d(&tout, stg, static_cast<int32_t>(c0), r0);
+            if (c0 + 32 < p.L) ptx::tma_store_2d(&tout, stg + 16384, static_cast<int32_t>(c0 + 32), r0);
+          }
+          ptx::bulk_commit();
+        }
+      }
+    }
+    if (leader) ptx::bulk_wait<0>();
+    // the tail past R rows (< L elements): scanned in fp64 by the last CTA
+    if (blockIdx.x == gridDim.x - 1) {
+      const long long base = p.R * p.L;
+      const long long ntail = (p.n - base + p.s - 1) / p.s;
+      OutT* out = reinterpret_cast<OutT*>(p.out);
+      for (long long j = et; j < ntail; j += kEpiThreads) {
+        const long long lo = base + j * p.s;
+        const long long hi = lo + p.s < p.n ? lo + p.s : p.n;
+        double run = 0.0;
+        for (long long e = lo; e < hi; ++e) {
+          const double y = in_to_float(p.x, e, p.in_bf16 != 0);
+          if (excl) {
+            out[e] = cvt_out_d<OutT>(run + 0.0);
+            run += y;
+          } else {
+            run += y;
+            out[e] = cvt_out_d<OutT>(run + 0.0);
+          }
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, kRssAcc * 64);
+  }
+}
+
+// =====================================================================
 // host side
 // =====================================================================
 
@@ -2216,15 +2854,16 @@ static DevInfo dev_info(int dev) {
 }
 
 static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base,
-                     long long rows, int box_cols) {
+                     long long rows, int box_cols, long long row_len = kRow,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(kRow), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(kRow) * esize};
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(row_len), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_len) * esize};
   cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(kTileRows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -2236,6 +2875,52 @@ static long long gcd_ll(long long a, long long b) {
     b = t;
   }
   return a;
+}
+
+// Segments per row for MODE_ROWSEG (0 = not applicable).  k is a power of
+// two times 8 / gcd(s, 8) (row pitch a multiple of 16 B), k outputs of at
+// most kRsMaxRowBytes per row (measured: 64 outputs per row ran at 54-63 %), with
+// the per-chunk B matrices within kRsMaxB; among those, the k with the
+// fewest 64-column chunks per element (a partly filled last chunk costs a
+// whole chunk's pipeline slot; measured on B200: rows of 40 elements run at
+// ~42 % of copy bandwidth, whole 64-column chunks at ~90 %).
+static int rowseg_k(long long s, long long n, int out_esize) {
+  if (s < 2 || s >= n) return 0;
+  if (gcd_ll(s, 64) > 8) return 0;  // >= 16-element granules: the GENERAL kernel is as fast
+  int best = 0;
+  double best_cost = 0.0;
+  for (long long k = 8 / gcd_ll(s, 8); k * out_esize <= kRsMaxRowBytes; k *= 2) {
+    const long long L = k * s;
+    const long long nch = (L + kRow - 1) / kRow;
+    const long long nn = k < 16 ? 16 : k;
+    if (nch * nn * 128 > static_cast<long long>(kRsMaxB)) break;
+    const double cost = static_cast<double>(nch) / static_cast<double>(L);
+    if (best == 0 || cost < best_cost * (1.0 - 1e-9)) {
+      best = static_cast<int>(k);
+      best_cost = cost;
+    }
+  }
+  return best;
+}
+
+// Segments per row for the MODE_ROWSEG scan (0 = not applicable): rows of
+// L = k s <= 64 kRssMaxChunks elements, k a power of two times 8 / gcd(s, 8),
+// the fewest chunks per element.  Only for the segment sizes whose granule
+// scan is slow (gcd(s, 64) <= 4: 16+ granules per row).
+static int rowseg_scan_k(long long s, long long n) {
+  if (s < 2 || s >= n) return 0;
+  if (gcd_ll(s, 64) > 4) return 0;
+  int best = 0;
+  double best_cost = 0.0;
+  for (long long k = 8 / gcd_ll(s, 8); k * s <= 64LL * kRssMaxChunks; k *= 2) {
+    const long long L = k * s;
+    const double cost = static_cast<double>((L + kRow - 1) / kRow) / static_cast<double>(L);
+    if (best == 0 || cost < best_cost * (1.0 - 1e-9)) {
+      best = static_cast<int>(k);
+      best_cost = cost;
+    }
+  }
+  return best;
 }
 
 // CHUNK arrays: units u = j*Gc + c < T + kMaxCtas, chunks j < T
@@ -2407,6 +3092,138 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
   return TC_OK;
 }
 
+template <typename OutT, int KS>
+static int launch_rowseg_k(const RsParams& p0, void* ws, cudaStream_t st) {
+  auto kern = rowseg_reduce_kernel<OutT, KS>;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::atomic<uint64_t> attr_done{0};
+  const uint64_t dev_bit = 1ull << (dev & 63);
+  if (!(attr_done.load() & dev_bit)) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kRsSmemMax) !=
+        cudaSuccess) {
+      set_err("cudaFuncSetAttribute failed: %s%lld", cudaGetErrorString(cudaGetLastError()), 0);
+      return TC_CUDA_ERROR;
+    }
+    attr_done.fetch_or(dev_bit);
+  }
+  const DevInfo di = dev_info(dev);
+  if (!di.ok || di.major < 10) {
+    set_err("no sm_100 device (compute capability major %s%lld)", "", di.major);
+    return TC_NO_DEVICE;
+  }
+  RsParams p = p0;
+  long long grid = 2LL * di.sms;  // 2 CTAs / SM (4-stage ring + B matrices)
+  if (grid > p.nblk) grid = p.nblk;
+  if (grid < 1) grid = 1;
+  CUtensorMap tin;
+  const char* wsb = reinterpret_cast<const char*>(ws);
+  const bool ok = p.R > 0
+      ? make_map(&tin, p.in_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                 2, p.x, p.R, kRow, p.L)
+      : make_map(&tin, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, wsb + kWsZeroRow, 1, kRow);
+  if (!ok) {
+    set_err("cuTensorMapEncodeTiled (row-segment input) failed%s%lld", "", 0);
+    return TC_CUDA_ERROR;
+  }
+  constexpr int kRowBytes = KS * static_cast<int>(sizeof(OutT));
+  CUtensorMap tout = tin;
+  if (kRowBytes >= 16 && p.R > 0) {
+    const CUtensorMapDataType dt = sizeof(OutT) == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                   : sizeof(OutT) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                       : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+    if (!make_map(&tout, dt, static_cast<int>(sizeof(OutT)), p.out, p.R, KS, KS,
+                  CU_TENSOR_MAP_SWIZZLE_NONE)) {
+      set_err("cuTensorMapEncodeTiled (row-segment output) failed%s%lld", "", 0);
+      return TC_CUDA_ERROR;
+    }
+  }
+  const uint32_t smem =
+      rs_off_misc(p.nchunk, rs_n(KS), kRowBytes >= 16 ? kRowBytes : 0) + sizeof(RsMisc) + 1024;
+  kern<<<static_cast<unsigned>(grid), kThreads, smem, st>>>(tin, tout, p);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_err("kernel launch failed: %s%lld", cudaGetErrorString(e), 0);
+    return TC_CUDA_ERROR;
+  }
+  ++g_launches;
+  return TC_OK;
+}
+
+template <typename OutT>
+static int launch_rowseg(const RsParams& p, void* ws, cudaStream_t st) {
+  switch (p.k) {
+    case 1: return launch_rowseg_k<OutT, 1>(p, ws, st);
+    case 2: return launch_rowseg_k<OutT, 2>(p, ws, st);
+    case 4: return launch_rowseg_k<OutT, 4>(p, ws, st);
+    case 8: return launch_rowseg_k<OutT, 8>(p, ws, st);
+    case 16: return launch_rowseg_k<OutT, 16>(p, ws, st);
+    case 32: return launch_rowseg_k<OutT, 32>(p, ws, st);
+  }
+  set_err("no row-segment kernel for %s%lld segments per row", "", p.k);
+  return TC_BAD_CONFIG;
+}
+
+template <typename OutT>
+static int launch_rowseg_scan(const RssParams& p0, void* ws, cudaStream_t st) {
+  auto kern = rowseg_scan_kernel<OutT>;
+  constexpr uint32_t smem = rss_smem<OutT>();
+  static_assert(smem <= 232448, "shared memory budget");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::atomic<uint64_t> attr_done{0};
+  const uint64_t dev_bit = 1ull << (dev & 63);
+  if (!(attr_done.load() & dev_bit)) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess) {
+      set_err("cudaFuncSetAttribute failed: %s%lld", cudaGetErrorString(cudaGetLastError()), 0);
+      return TC_CUDA_ERROR;
+    }
+    attr_done.fetch_or(dev_bit);
+  }
+  const DevInfo di = dev_info(dev);
+  if (!di.ok || di.major < 10) {
+    set_err("no sm_100 device (compute capability major %s%lld)", "", di.major);
+    return TC_NO_DEVICE;
+  }
+  RssParams p = p0;
+  long long grid = di.sms;
+  if (grid > p.nblk) grid = p.nblk;
+  if (grid < 1) grid = 1;
+  CUtensorMap tin, tout;
+  const char* wsb = reinterpret_cast<const char*>(ws);
+  const bool fp16 = sizeof(OutT) == 2;
+  bool ok;
+  if (p.R > 0) {
+    ok = make_map(&tin, p.in_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                  2, p.x, p.R, kRow, p.L) &&
+         (fp16 ? make_map(&tout, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, p.out, p.R, kRow, p.L)
+               : make_map(&tout, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.out, p.R, 32, p.L));
+  } else {
+    ok = make_map(&tin, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, wsb + kWsZeroRow, 1, kRow) &&
+         make_map(&tout, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, wsb + kWsDummyOut, 1, kRow);
+  }
+  if (!ok) {
+    set_err("cuTensorMapEncodeTiled (row-segment scan) failed%s%lld", "", 0);
+    return TC_CUDA_ERROR;
+  }
+  kern<<<static_cast<unsigned>(grid), kThreads, smem, st>>>(tin, tout, p);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_err("kernel launch failed: %s%lld", cudaGetErrorString(e), 0);
+    return TC_CUDA_ERROR;
+  }
+  ++g_launches;
+  return TC_OK;
+}
+
+static bool rowseg_enabled() {
+  const char* e = getenv("TC_ROWSEG");  // tuning / A-B switch
+  return !(e && e[0] == '0');
+}
+
 using LaunchFn = int (*)(const Params&, int, cudaStream_t);
 
 template <int OP, int MODE, typename OutT>
@@ -2562,6 +3379,25 @@ int tc_seg_reduce_ex(const void* x, int in_dtype, int64_t n, int64_t seg, void* 
     set_err("unsupported input dtype %s%lld", "", in_dtype);
     return TC_BAD_CONFIG;
   }
+  const int out_es = out_dtype == TC_F16 ? 2 : out_dtype == TC_F32 ? 4 : 8;
+  if (const int k = rowseg_enabled() ? rowseg_k(seg, n, out_es) : 0) {
+    // whole segments per TMA row (MODE_ROWSEG): no carries at all
+    RsParams rp{};
+    rp.x = reinterpret_cast<const __half*>(x);
+    rp.in_bf16 = (in_dtype == TC_BF16) ? 1 : 0;
+    rp.out = out;
+    rp.n = n;
+    rp.s = seg;
+    rp.k = k;
+    rp.L = static_cast<long long>(k) * seg;
+    rp.R = n / rp.L;
+    rp.nblk = (rp.R + kTileRows - 1) / kTileRows;
+    rp.nchunk = static_cast<int>((rp.L + kRow - 1) / kRow);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    return out_dtype == TC_F16   ? launch_rowseg<__half>(rp, ws, st)
+           : out_dtype == TC_F32 ? launch_rowseg<float>(rp, ws, st)
+                                 : launch_rowseg<double>(rp, ws, st);
+  }
   int gr = 0, mode = 0;
   Params p = make_params(x, n, seg, out, ws, TC_OP_REDUCE, false, &gr, &mode);
   p.in_bf16 = (in_dtype == TC_BF16) ? 1 : 0;
@@ -2603,6 +3439,25 @@ int tc_seg_scan_ex(const void* x, int in_dtype, int64_t n, int64_t seg, void* ou
   if (in_dtype != TC_F16 && in_dtype != TC_BF16) {
     set_err("unsupported input dtype %s%lld", "", in_dtype);
     return TC_BAD_CONFIG;
+  }
+  if (carry_in == nullptr && total_out == nullptr) {
+    if (const int k = rowseg_enabled() ? rowseg_scan_k(seg, n) : 0) {
+      // whole segments per TMA row (MODE_ROWSEG): no carries between rows
+      RssParams rp{};
+      rp.x = reinterpret_cast<const __half*>(x);
+      rp.in_bf16 = (in_dtype == TC_BF16) ? 1 : 0;
+      rp.out = out;
+      rp.n = n;
+      rp.s = seg;
+      rp.L = static_cast<long long>(k) * seg;
+      rp.R = n / rp.L;
+      rp.nblk = (rp.R + kTileRows - 1) / kTileRows;
+      rp.nchunk = static_cast<int>((rp.L + kRow - 1) / kRow);
+      rp.exclusive = exclusive ? 1 : 0;
+      cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+      return out_dtype == TC_F16 ? launch_rowseg_scan<__half>(rp, ws, st)
+                                 : launch_rowseg_scan<float>(rp, ws, st);
+    }
   }
   int gr = 0, mode = 0;
   Params p = make_params(x, n, seg, out, ws, TC_OP_SCAN, carry_in != nullptr, &gr, &mode);
@@ -2731,24 +3586,62 @@ int tc_bn_stats(const void* x, int in_dtype, int64_t N, int64_t C, int64_t HW, v
     return TC_NO_DEVICE;
   }
   const long long nsegs = N * C;
-  long long blocks = (nsegs + kBnThreads / 32 - 1) / (kBnThreads / 32);
-  const long long cap = static_cast<long long>(di.sms) * (2048 / kBnThreads);  // one wave
-  if (blocks > cap) blocks = cap;
   const __half* xh = reinterpret_cast<const __half*>(x);
   const int bf = in_dtype == TC_BF16 ? 1 : 0;
-  bn_moments_kernel<<<static_cast<unsigned>(blocks), kBnThreads, 0, st>>>(xh, bf, N, C, HW, mom);
+  long long groups = N;
+  if (HW % 8 == 0 && HW >= kBnChanMin) {
+    // per-channel blocks over sample ranges: ~8 blocks per SM
+    long long splits = (8LL * di.sms + C - 1) / C;
+    if (splits > N) splits = N;
+    if (splits > 65535) splits = 65535;
+    groups = splits;
+    bn_chan_kernel<<<dim3(static_cast<unsigned>(C), static_cast<unsigned>(splits)), kBnThreads, 0,
+                     st>>>(xh, bf, N, C, HW, mom);
+  } else {
+    const long long per_block = HW < kBnWarpMin ? kBnThreads : kBnThreads / 32;  // segments
+    long long blocks = (nsegs + per_block - 1) / per_block;
+    const long long cap = static_cast<long long>(di.sms) * (2048 / kBnThreads);  // one wave
+    if (blocks > cap) blocks = cap;
+    bn_moments_kernel<<<static_cast<unsigned>(blocks), kBnThreads, 0, st>>>(xh, bf, N, C, HW, mom);
+  }
   if (out_dtype == TC_F32)
     bn_finish_kernel<float><<<static_cast<unsigned>(C), kBnThreads, 0, st>>>(
-        xh, bf, N, C, HW, mom, reinterpret_cast<float*>(mean), reinterpret_cast<float*>(var));
+        xh, bf, N, C, HW, mom, groups, reinterpret_cast<float*>(mean), reinterpret_cast<float*>(var));
   else
     bn_finish_kernel<double><<<static_cast<unsigned>(C), kBnThreads, 0, st>>>(
-        xh, bf, N, C, HW, mom, reinterpret_cast<double*>(mean), reinterpret_cast<double*>(var));
+        xh, bf, N, C, HW, mom, groups, reinterpret_cast<double*>(mean),
+        reinterpret_cast<double*>(var));
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_err("kernel launch failed: %s%lld", cudaGetErrorString(e), 0);
     return TC_CUDA_ERROR;
   }
   g_launches += 2;
+  return TC_OK;
+}
+
+int tc_plan_info(int op, int64_t n, int64_t seg, int out_dtype, int has_carry, int has_total,
+                 int* mode, int64_t* row_len) {
+  if (n < 1 || seg < 1 || (op != TC_OP_REDUCE && op != TC_OP_SCAN) || !mode || !row_len)
+    return TC_BAD_CONFIG;
+  const int es = out_dtype == TC_F16 ? 2 : out_dtype == TC_F32 ? 4 : 8;
+  int k = 0;
+  if (rowseg_enabled()) {
+    if (op == TC_OP_REDUCE)
+      k = rowseg_k(seg, n, es);
+    else if (!has_carry && !has_total)
+      k = rowseg_scan_k(seg, n);
+  }
+  if (k) {
+    *mode = MODE_ROWSEG;
+    *row_len = static_cast<int64_t>(k) * seg;
+    return TC_OK;
+  }
+  static char dummy[1024];
+  int gr = 0, md = 0;
+  make_params(dummy, n, seg, dummy, dummy, op, op == TC_OP_SCAN && has_carry, &gr, &md);
+  *mode = md;
+  *row_len = kRow;
   return TC_OK;
 }
 
@@ -2770,6 +3663,6 @@ const char* tc_last_error(void) { return g_err; }
 uint64_t tc_launch_count(void) { return g_launches; }
 void tc_reset_launch_count(void) { g_launches = 0; }
 
-int tc_abi_version(void) { return (1 << 16) | 3; }
+int tc_abi_version(void) { return (1 << 16) | 4; }
 
 }  // extern "C"

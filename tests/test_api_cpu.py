@@ -248,3 +248,25 @@ def test_batchnorm_validation_before_device():
 def test_batch_norm_forward_needs_cuda_tensor():
     with pytest.raises(TypeError):
         ht.batch_norm(np.ones((2, 3, 4), np.float16))
+
+
+def test_plan_info_modes():
+    """tc_plan_info mirrors the dispatch (host only): which kernel runs."""
+    import torch
+
+    from paper_1811_09736_b200 import _device as D
+
+    n = 1 << 30
+    assert D.plan_info("reduce", n, 16) == ("LOCAL", 64)
+    assert D.plan_info("reduce", n, 256) == ("ROWS", 64)
+    assert D.plan_info("reduce", n, 65536) == ("TILES", 64)
+    assert D.plan_info("reduce", n, 48) == ("GENERAL", 64)
+    mode, L = D.plan_info("reduce", n, 3)
+    assert mode == "ROWSEG" and L % 3 == 0 and (2 * L) % 16 == 0
+    mode, L = D.plan_info("reduce", n, 3, torch.float32)
+    assert mode == "ROWSEG" and (L // 3) * 4 <= 64
+    assert D.plan_info("reduce", n, 100001)[0] == "GENERAL"
+    assert D.plan_info("scan", n, n)[0] == "CHUNK"
+    assert D.plan_info("scan", n, 4096, carry_in=True)[0] == "CHUNK"
+    assert D.plan_info("scan", n, 17)[0] == "ROWSEG"
+    assert D.plan_info("scan", n, 17, total_out=True)[0] == "GENERAL"

@@ -148,7 +148,7 @@ def test_signed_scan_every_mode(kind, data):
 @pytest.mark.parametrize("kind", ["int", "uniform_pm1", "mixed_mag"])
 def test_signed_carry_in_total_out(kind, data, cuda):
     """CHUNK mode with a carry-in (the multi-GPU full-scan building block):
-    outputs bounded as above (the carry counts as exact); total_out comes
+    outputs bounded as above (the carry counts as one more summand); total_out comes
     from the fp64 carry chain, so its only error is the fp32 accumulation of
     the in-row / in-tile pieces: bounded by GAMMA * A with no output
     rounding (and exact on integer data)."""
@@ -159,7 +159,9 @@ def test_signed_carry_in_total_out(kind, data, cuda):
     ax = np.abs(x)
     for exc in (False, True):
         exact = O.ref_seg_scan(x, N, inclusive=not exc, carry=carry)
-        mass = O.ref_seg_scan(ax, N, inclusive=not exc)
+        # the caller's carry is one more summand of every output (its value
+        # enters the kernel's fp64 chain and is rounded with the offset)
+        mass = O.ref_seg_scan(ax, N, inclusive=not exc) + abs(carry)
         got = D.seg_scan(xd, N, torch.float32, exclusive=exc, carry_in=cin, total_out=tot)
         got = got.cpu().numpy()
         if kind == "int":
@@ -239,44 +241,64 @@ def test_neighbour_magnitude_isolation(cuda):
 # ------------------------------------------------------------ non-finite data
 
 
+def _poison_units(pos, n, s, op):
+    """[lo, hi) of the MMA row accumulation each non-finite position feeds
+    (tc_plan_info): the 64-element row, or for MODE_ROWSEG (rows of L = k s
+    whole segments) the whole L-row (reduce) / its 64-column chunk (scan).
+    Positions past the last full row (the ragged tail, CUDA cores) feed none."""
+    mode, L = D.plan_info(op, n, s, torch.float32)
+    units = set()
+    for p in pos:
+        r = p // L
+        if (r + 1) * L > n:
+            continue
+        if mode == "ROWSEG" and op == "scan":
+            c = (p - r * L) // 64
+            units.add((r * L + 64 * c, min(r * L + 64 * c + 64, (r + 1) * L)))
+        else:
+            units.add((r * L, (r + 1) * L))
+    return sorted(units)
+
+
 def test_nonfinite_contamination_rule(cuda):
     """Documented B200 semantics for NaN / +-Inf inputs (DESIGN.md section 5;
     the reference: engine.py:344-348 -- NaN*0 and Inf*0 in the tile MMA
-    poison the whole 16-wide tile row).  Here the MMA row is 64 elements, so
-    a non-finite x[i] poisons its 64-element row r = i // 64:
+    poison the whole 16-wide tile row).  Here a non-finite x[i] poisons the
+    MMA row accumulation it feeds (tc_plan_info): its 64-element row, or in
+    the whole-segments-per-row kernels (MODE_ROWSEG) the row of k segments
+    (reduce) / the row's 64-column chunk (scan):
 
     * an output whose exact value involves a non-finite element is non-finite;
     * every other output is exact, or -- only inside the poison zone -- non-
       finite.  The zone: for a reduce, the segments that overlap a poisoned
-      row; for a scan, output i when some poisoned row r overlaps i's segment
-      and 64 r <= i (the row itself, and the rest of every segment running
-      through it; CTAs that re-derive their entry carry from HBM on CUDA
-      cores may return the exact value instead).  An exclusive scan's
+      unit; for a scan, output i when a poisoned unit [lo, hi) overlaps i's
+      segment and lo <= i (the unit itself, and the rest of every segment
+      running through it; CTAs that re-derive their entry carry from HBM on
+      CUDA cores may return the exact value instead).  An exclusive scan's
       segment-start outputs are always 0.
 
-    (The ragged last row, n % 64 elements, is summed on CUDA cores and
-    follows exact-arithmetic contamination; the test keeps it finite.)"""
+    (The ragged tail past the last full row is summed on CUDA cores and
+    follows exact-arithmetic contamination.)"""
     rng = np.random.default_rng(11)
     n = (1 << 20) + 100
     x = rng.integers(-8, 8, n).astype(np.float16)
-    bad_at = np.sort(rng.choice((n // 64) * 64 - 1, 24, replace=False))
+    bad_at = np.sort(rng.choice(n, 24, replace=False))
     x[bad_at[0::3]] = np.nan
     x[bad_at[1::3]] = np.inf
     x[bad_at[2::3]] = -np.inf
     xd = torch.from_numpy(x).to(cuda)
     nf = ~np.isfinite(x.astype(np.float32))
-    row_lo = np.unique(bad_at // 64) * 64
     clean = np.where(nf, 0, x).astype(np.float16)
     i = np.arange(n)
     nf_count = np.concatenate([[0], np.cumsum(nf)])  # non-finite elements before position j
-    for s in (16, 64, 256, 3, 48, 300, 16384, 8192 * 3, 100001, (1 << 18) + 8192, n):
+    for s in (16, 64, 256, 3, 7, 17, 48, 300, 16384, 8192 * 3, 100001, (1 << 18) + 8192, n):
         nseg = -(-n // s)
         starts = np.arange(nseg) * s
         ends = np.minimum(starts + s, n)
-        zone = np.zeros(nseg, bool)
-        for lo in row_lo:
-            zone |= (starts < lo + 64) & (ends > lo)
         must = (nf_count[ends] - nf_count[starts]) > 0
+        zone = must.copy()
+        for lo, hi in _poison_units(bad_at, n, s, "reduce"):
+            zone |= (starts < hi) & (ends > lo)
         got = D.seg_reduce(xd, s, torch.float32).cpu().numpy()
         exp = O.ref_seg_reduce(clean, s).astype(np.float32)
         fin = np.isfinite(got)
@@ -284,14 +306,15 @@ def test_nonfinite_contamination_rule(cuda):
         assert np.array_equal(got[fin], exp[fin]), ("reduce: finite outputs exact", s)
         assert zone[~fin].all(), ("reduce: non-finite outside the zone", s)
         seg_start = (i // s) * s
-        pz = np.zeros(n, bool)
-        for lo in row_lo:
-            pz |= (i >= lo) & (seg_start < lo + 64)
+        units = _poison_units(bad_at, n, s, "scan")
         for exc in (False, True):
             got = D.seg_scan(xd, s, torch.float32, exclusive=exc).cpu().numpy()
             exp = O.ref_seg_scan(clean, s, inclusive=not exc).astype(np.float32)
             upto = i + 1 if not exc else i
             must = (nf_count[upto] - nf_count[seg_start]) > 0
+            pz = must.copy()
+            for lo, hi in units:
+                pz |= (i >= lo) & (seg_start < hi)
             fin = np.isfinite(got)
             if exc:
                 assert np.all(got[i % s == 0] == 0), ("excl starts", s)

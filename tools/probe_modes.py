@@ -44,22 +44,34 @@ def main():
     x = torch.rand(n, device=dev, dtype=torch.float32).to(torch.float16)
     which = sys.argv[1:] or ["reduce", "scan", "bn"]
     if "reduce" in which:
-        for s in [3, 5, 7, 9, 12, 17, 20, 24, 33, 40, 48, 49, 63, 65, 100, 127, 300, 1000, 4097,
-                  100001]:
+        import os
+
+        for s in [3, 5, 7, 9, 12, 17, 20, 24, 33, 40, 48, 49, 63, 65, 100, 127, 129, 300, 1000,
+                  4097, 100001]:
             for dt, o in ((torch.float16, 2), (torch.float32, 4)):
                 out = torch.empty(-(-n // s), dtype=dt, device=dev)
-                ms = timeit(lambda: D.seg_reduce(x, s, dt, out=out))
-                gbs = (2 * n + o * (-(-n // s))) / ms / 1e6
-                print(f"reduce s={s:>7} {str(dt):14} {ms:7.3f} ms {gbs:6.0f} GB/s "
-                      f"{100 * gbs / PEAK:5.1f}%", flush=True)
+                res = []
+                for rs in ("1", "0"):  # MODE_ROWSEG on / off (A/B in one process)
+                    os.environ["TC_ROWSEG"] = rs
+                    ms = timeit(lambda: D.seg_reduce(x, s, dt, out=out))
+                    gbs = (2 * n + o * (-(-n // s))) / ms / 1e6
+                    res.append(f"rowseg={rs} {ms:7.3f} ms {gbs:6.0f} GB/s {100 * gbs / PEAK:5.1f}%")
+                os.environ.pop("TC_ROWSEG")
+                print(f"reduce s={s:>7} {str(dt):14} " + " | ".join(res), flush=True)
     if "scan" in which:
-        for s in [3, 7, 17, 48, 300, 1000, 100001, (1 << 19) + 3, n]:
+        import os
+
+        for s in [3, 5, 7, 9, 12, 17, 20, 33, 48, 63, 65, 100, 300, 1000, 100001, (1 << 19) + 3, n]:
             for dt, o in ((torch.float16, 2), (torch.float32, 4)):
                 out = torch.empty(n, dtype=dt, device=dev)
-                ms = timeit(lambda: D.seg_scan(x, s, dt, out=out))
-                gbs = (2 + o) * n / ms / 1e6
-                print(f"scan   s={s:>10} {str(dt):14} {ms:7.3f} ms {gbs:6.0f} GB/s "
-                      f"{100 * gbs / PEAK:5.1f}%", flush=True)
+                res = []
+                for rs in ("1", "0"):
+                    os.environ["TC_ROWSEG"] = rs
+                    ms = timeit(lambda: D.seg_scan(x, s, dt, out=out))
+                    gbs = (2 + o) * n / ms / 1e6
+                    res.append(f"rowseg={rs} {ms:7.3f} ms {gbs:6.0f} GB/s {100 * gbs / PEAK:5.1f}%")
+                os.environ.pop("TC_ROWSEG")
+                print(f"scan   s={s:>10} {str(dt):14} " + " | ".join(res), flush=True)
     if "bn" in which:
         for shape in ((256, 256, 56, 56), (256, 512, 28, 28), (256, 1024, 14, 14),
                       (256, 2048, 7, 7)):
