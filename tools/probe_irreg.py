@@ -1,5 +1,6 @@
 """Iteration aid: irregular (CSR-offset) reduce / scan bandwidth at 2^30 fp16
 with geometric segment lengths of the given means."""
+import os
 import sys
 
 import torch
@@ -37,6 +38,8 @@ def main():
             gbs = byts / ms / 1e6
             print(f"irreg reduce mean={mean:>8} nseg={nseg:>9} {str(dt):14} {ms:8.3f} ms {gbs:7.0f} GB/s "
                   f"{100 * gbs / PEAK:5.1f}%", flush=True)
+        if os.environ.get("PROBE_REDUCE_ONLY"):
+            continue
         for dt, o in ((torch.float32, 4), (torch.float16, 2)):
             out = torch.empty(n, dtype=dt, device=dev)
             ms = timeit(lambda: D.irreg_scan(x, off, dt, out=out, validate=False))
