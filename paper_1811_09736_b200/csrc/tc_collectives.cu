@@ -95,6 +95,10 @@ constexpr int MODE_GENERAL = 3;
 constexpr int MODE_CHUNK = 4;
 constexpr int MODE_IRREG = 5;  // irregular segments from a CSR offsets array
 constexpr int MODE_ROWSEG = 7;  // whole segments per TMA row (rowseg_*_kernel)
+// scan with at most one segment start per row and few factors of two
+// (seg >= 64, gcd(seg, 64) <= 4): granules of 8 (GR = 8) with the one
+// granule that a start splits recomputed from its raw elements
+constexpr int MODE_SPLIT = 8;
 constexpr int MODE_GSCR = 6;   // GENERAL reduce with many segment ends per row (2m < GR):
                                // end values staged in SMEM, interior segments stored coalesced
 constexpr int kMaxCtas = 1024;                    // persistent grid cap
@@ -114,7 +118,12 @@ struct Entry {  // one cross-CTA partial of a reduce
 constexpr size_t kWsZeroRow = 256;   // 256 B of zeros: TMA source when R == 0
 constexpr size_t kWsDummyOut = 512;  // 512 B scratch: TMA store target when R == 0
 constexpr size_t kWsEntries = 1024;
-constexpr size_t kWsLookback = kWsEntries + sizeof(Entry) * 2 * kMaxCtas;
+// per-channel arrival tickets of the batch-norm statistics: a region no other
+// op writes, so it stays zero between calls (the last block resets its
+// channel's ticket)
+constexpr size_t kWsBnTickets = kWsEntries + sizeof(Entry) * 2 * kMaxCtas;
+constexpr long long kBnMaxTicketC = 2048;
+constexpr size_t kWsLookback = kWsBnTickets + sizeof(unsigned) * kBnMaxTicketC;
 
 struct Params {
   const __half* x;      // input bits (binary16, or bfloat16 when in_bf16)
@@ -195,7 +204,8 @@ struct Cfg {
   // fp32-output scans at 2 CTAs/SM fit either 4 input stages + 1 output
   // buffer or 2 + 2.  The pair-scan modes (GENERAL, IRREG) prefer 2 + 2
   // (measured: s = 300 79 -> 87 % of copy bandwidth), the others 4 + 1.
-  static constexpr bool SCAN32_2BUF = (MODE == MODE_GENERAL || MODE == MODE_IRREG);
+  static constexpr bool SCAN32_2BUF =
+      (MODE == MODE_GENERAL || MODE == MODE_IRREG || MODE == MODE_SPLIT);
   static constexpr int STAGES = CHUNK ? 8
                                 : (OP == OP_REDUCE)
                                     ? ((MINB == 3 || MODE == MODE_GSCR || MODE == MODE_IRREG) ? 4
@@ -358,9 +368,7 @@ __device__ double epi_range_sum(const __half* x, bool bf16, long long lo, long l
     const long long nb = (hi - a) >> 3;  // whole 8-element blocks
     const uint4* xv = reinterpret_cast<const uint4*>(x + a);
     float fs = 0.f;
-    int cnt = 0;
-    for (long long b = et; b < nb; b += kEpiThreads) {
-      const uint4 w = __ldg(xv + b);
+    auto add8 = [&](const uint4& w) {
       if (bf16) {
         const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
 #pragma unroll
@@ -376,12 +384,21 @@ __device__ double epi_range_sum(const __half* x, bool bf16, long long lo, long l
           fs += f2.x + f2.y;
         }
       }
-      if (++cnt == 64) {  // flush to fp64 every 512 elements
-        acc += fs;
-        fs = 0.f;
-        cnt = 0;
-      }
+    };
+    // eight 16-B loads in flight per thread (this pass can be ~2^21 elements
+    // per CTA: one load at a time made it latency-bound); fp32 partials go
+    // to fp64 every 8 x 8 elements
+    long long b = et;
+    for (; b + 7 * kEpiThreads < nb; b += 8 * kEpiThreads) {
+      uint4 w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) w[u] = __ldg(xv + b + u * kEpiThreads);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) add8(w[u]);
+      acc += fs;
+      fs = 0.f;
     }
+    for (; b < nb; b += kEpiThreads) add8(__ldg(xv + b));
     acc += fs;
     if (et == kEpiThreads - 1)
       for (long long e = a + nb * 8; e < hi; ++e) acc += in_to_float(x, e, bf16);
@@ -805,66 +822,136 @@ __global__ void __launch_bounds__(kBnThreads) bn_moments_kernel(const __half* x,
     run(std::integral_constant<int, 1>{});
 }
 
-// Long, 16-byte aligned segments (HW % 8 == 0, HW >= kBnChanMin): block
-// (c, sp) streams channel c of samples [n0, n1) -- a flat index over the
-// 8-element vectors of those segments, four 16-byte loads in flight per
-// thread -- and accumulates ONE (S1, S2) pair for the channel (every element
-// shares K_c), so the scratch is [splits][C] instead of [N][C].
-constexpr long long kBnChanMin = 512;
+// Per-channel streaming (HW >= kBnChanMin): block (c, sp) streams channel c
+// of samples [n0, n1) as ONE flat index over the V-element vectors of those
+// segments (V = 8 / 4 / 2 / 1 by the segment alignment; consecutive threads
+// read consecutive vectors), four loads in flight per thread, and
+// accumulates ONE (S1, S2) pair for the channel (every element shares K_c),
+// so the scratch is [splits][C] instead of [N][C].  The flat index is split
+// into (segment, vector) with a 32-bit multiply-shift division (the 64-bit
+// division it replaces dominated the issue slots), and the moments use the
+// packed fp32x2 pipe (FADD2 / FFMA2): two elements per instruction.
+constexpr long long kBnChanMin = 48;
 
+struct FastDiv {  // q = floor(i / d) for 0 <= i < 2^31, 1 <= d < 2^31
+  uint32_t d, mul, shr;
+};
+static FastDiv make_fastdiv(uint32_t d) {
+  uint32_t shr = 0;
+  while ((1ull << shr) < d) ++shr;
+  const uint64_t mul = ((1ull << 32) * ((1ull << shr) - d)) / d + 1;
+  return FastDiv{d, static_cast<uint32_t>(mul), shr};
+}
+__device__ __forceinline__ uint32_t fastdiv(uint32_t i, const FastDiv& f) {
+  return (__umulhi(i, f.mul) + i) >> f.shr;
+}
+
+template <int V, typename OutT>
 __global__ void __launch_bounds__(kBnThreads) bn_chan_kernel(const __half* x, int in_bf16,
                                                              long long N, long long C,
-                                                             long long HW, double2* mom) {
+                                                             long long HW, FastDiv fd,
+                                                             double2* mom, unsigned* ticket,
+                                                             OutT* mean_out, OutT* var_out) {
+  using VT = typename std::conditional<V == 8, uint4,
+             typename std::conditional<V == 4, uint2,
+             typename std::conditional<V == 2, uint32_t, unsigned short>::type>::type>::type;
   __shared__ double sred[kBnThreads / 32];
   const long long c = blockIdx.x;
   const int splits = gridDim.y, sp = blockIdx.y;
   const long long n0 = N * sp / splits, n1 = N * (sp + 1) / splits;
   const bool bf16 = in_bf16 != 0;
   const float k = in_to_float(x, c * HW, bf16);
-  const long long nv = HW / 8;                  // vectors per segment
-  const long long total = (n1 - n0) * nv;
-  const uint4* base = reinterpret_cast<const uint4*>(x);
-  auto addr = [&](long long i) -> long long {  // vector index in x of flat vector i
-    const long long q = i / nv;
-    return ((n0 + q) * C + c) * nv + (i - q * nv);
+  const float2 nk = make_float2(-k, -k);
+  const uint32_t nv = fd.d;  // vectors per segment (HW / V)
+  const uint32_t total = static_cast<uint32_t>((n1 - n0) * nv);
+  const VT* base = reinterpret_cast<const VT*>(x) + (n0 * C + c) * static_cast<long long>(nv);
+  const long long sstride = C * static_cast<long long>(nv);  // vectors between samples
+  auto ld = [&](uint32_t i) -> VT {
+    const uint32_t q = fastdiv(i, fd);
+    return __ldcs(base + q * sstride + (i - q * nv));
   };
-  float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
-  auto acc = [&](const uint4& w, int u) {
-    const unsigned short* h = reinterpret_cast<const unsigned short*>(&w);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float f = bf16 ? __uint_as_float(static_cast<uint32_t>(h[e]) << 16)
-                           : __half2float(__ushort_as_half(h[e]));
+  float2 s1[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  float2 s2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  float tail1 = 0.f, tail2 = 0.f;  // V == 1
+  auto acc = [&](const VT& w, int u) {
+    if constexpr (V == 1) {
+      const float f = bf16 ? __uint_as_float(static_cast<uint32_t>(w) << 16)
+                           : __half2float(__ushort_as_half(w));
       const float a = f - k;
-      s1[u] += a;
-      s2[u] = fmaf(a, a, s2[u]);
+      tail1 += a;
+      tail2 = fmaf(a, a, tail2);
+    } else {
+      const uint32_t* h = reinterpret_cast<const uint32_t*>(&w);
+#pragma unroll
+      for (int e = 0; e < V / 2; ++e) {
+        const float2 f = bf16 ? make_float2(__uint_as_float(h[e] << 16),
+                                            __uint_as_float(h[e] & 0xffff0000u))
+                              : __half22float2(*reinterpret_cast<const __half2*>(&h[e]));
+        const float2 a = ptx::add_f32x2(f, nk);
+        s1[u] = ptx::add_f32x2(s1[u], a);
+        s2[u] = ptx::fma_f32x2(a, a, s2[u]);
+      }
     }
   };
   double d1 = 0.0, d2 = 0.0;
-  const long long step = blockDim.x;
-  long long i = threadIdx.x;
+  auto flush = [&]() {
+    d1 += (static_cast<double>(s1[0].x) + s1[0].y) + (static_cast<double>(s1[1].x) + s1[1].y) +
+          static_cast<double>(tail1);
+    d2 += (static_cast<double>(s2[0].x) + s2[0].y) + (static_cast<double>(s2[1].x) + s2[1].y) +
+          static_cast<double>(tail2);
+    s1[0] = s1[1] = s2[0] = s2[1] = make_float2(0.f, 0.f);
+    tail1 = tail2 = 0.f;
+  };
+  constexpr uint32_t step = kBnThreads;
+  uint32_t i = threadIdx.x;
   int it = 0;
   for (; i + 3 * step < total; i += 4 * step) {
-    const uint4 a = __ldcs(base + addr(i)), b = __ldcs(base + addr(i + step)),
-                cc = __ldcs(base + addr(i + 2 * step)), d = __ldcs(base + addr(i + 3 * step));
+    const VT a = ld(i), b = ld(i + step), cc = ld(i + 2 * step), d = ld(i + 3 * step);
     acc(a, 0);
     acc(b, 1);
-    acc(cc, 2);
-    acc(d, 3);
-    if (++it == 16) {  // flush the fp32 partials to fp64 every 512 elements per slot
-      d1 += (static_cast<double>(s1[0]) + s1[1]) + (static_cast<double>(s1[2]) + s1[3]);
-      d2 += (static_cast<double>(s2[0]) + s2[1]) + (static_cast<double>(s2[2]) + s2[3]);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) s1[u] = s2[u] = 0.f;
+    acc(cc, 0);
+    acc(d, 1);
+    if (++it == 64 / V) {  // fp32 partials to fp64 every 128 elements per slot
+      flush();
       it = 0;
     }
   }
-  for (; i < total; i += step) acc(__ldcs(base + addr(i)), 0);
-  d1 += (static_cast<double>(s1[0]) + s1[1]) + (static_cast<double>(s1[2]) + s1[3]);
-  d2 += (static_cast<double>(s2[0]) + s2[1]) + (static_cast<double>(s2[2]) + s2[3]);
+  for (; i < total; i += step) acc(ld(i), 0);
+  flush();
   const double t1 = block_sum_d(d1, sred);
   const double t2 = block_sum_d(d2, sred);
-  if (threadIdx.x == 0) mom[static_cast<long long>(sp) * C + c] = make_double2(t1, t2);
+  // the channel's last block to finish combines the splits' moments in
+  // split order (deterministic) -- no second launch -- and re-zeroes the
+  // scratch and the ticket for the next call
+  __shared__ int last;
+  if (threadIdx.x == 0) {
+    mom[static_cast<long long>(sp) * C + c] = make_double2(t1, t2);
+    __threadfence();
+    last = (atomicAdd(&ticket[c], 1u) == static_cast<unsigned>(splits - 1));
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < 32) {
+    double a1 = 0.0, a2 = 0.0;
+    for (int g = threadIdx.x; g < splits; g += 32) {  // lane-strided, then a fixed tree
+      const double2 m = __ldcg(&mom[static_cast<long long>(g) * C + c]);
+      a1 += m.x;
+      a2 += m.y;
+      mom[static_cast<long long>(g) * C + c] = make_double2(0.0, 0.0);
+    }
+    a1 = warp_sum_d(a1);
+    a2 = warp_sum_d(a2);
+    if (threadIdx.x == 0) {
+      const double m = static_cast<double>(N * HW);
+      const double dm = a1 / m;  // mean - K
+      double var = a2 / m - dm * dm;
+      if (var < 0.0) var = 0.0;
+      mean_out[c] = static_cast<OutT>(static_cast<double>(k) + dm);
+      var_out[c] = static_cast<OutT>(var);
+      ticket[c] = 0u;  // ready for the next call
+    }
+  }
 }
 
 template <typename OutT>
@@ -971,7 +1058,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
     if (OP == OP_SCAN) ptx::prefetch_tmap(&tout);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&misc->full[s], 1);
-      ptx::mbar_init(&misc->empty[s], 1);
+      ptx::mbar_init(&misc->empty[s], MODE == MODE_SPLIT ? 4 : 1);  // SPLIT: the 4 epilogue warps
     }
     for (int a = 0; a < ACC; ++a) {
       ptx::mbar_init(&misc->tfull[a], 1);
@@ -1031,7 +1118,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
 #pragma unroll
         for (int k = 0; k < 4; ++k)  // K = 64 = 4 x 16; +32 B per K step inside the SW128 atom
           ptx::mma_f16_ss(tmem + a * N, adesc + 2 * k, bdesc + 2 * k, idesc, k > 0 ? 1u : 0u);
-        ptx::mma_commit(&misc->empty[s]);
+        if constexpr (MODE != MODE_SPLIT) ptx::mma_commit(&misc->empty[s]);  // SPLIT: the epilogue frees it
         ptx::mma_commit(&misc->tfull[a]);
       });
     }
@@ -1056,11 +1143,17 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
       qmod = q0 % p.m;
       qdiv = q0 / p.m;
     }
+    if constexpr (MODE == MODE_SPLIT) {  // element granularity: the row's first element mod seg
+      const long long e0 = (t_begin * kTileRows + rit) * kRow;
+      qmod = e0 % p.m;
+      qdiv = e0 / p.m;
+    }
     if constexpr (MODE == MODE_TILES) {
       tpos = t_begin % p.ktiles;
       tseg = t_begin / p.ktiles;
     }
-    if constexpr (OP == OP_SCAN && (MODE == MODE_TILES || MODE == MODE_GENERAL)) {
+    if constexpr (OP == OP_SCAN &&
+                  (MODE == MODE_TILES || MODE == MODE_GENERAL || MODE == MODE_SPLIT)) {
       // carry entering this CTA's range: the (< seg) elements of the open
       // segment that precede the range, re-read from HBM (bounded by
       // kScanPrepassMax), plus the caller's carry for segment 0.
@@ -1216,6 +1309,13 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
           vv[k] = s;
         }
       }
+    };
+    // SPLIT: segment start column of this thread's row in tile tt (64 =
+    // none; qm = the row's first element mod seg)
+    auto split_start = [&](long long tt, long long qm) -> int {
+      const long long rowpos = (tt * kTileRows + rit) * kRow;
+      const long long r0 = qm == 0 ? 0 : p.m - qm;
+      return (r0 < kRow && rowpos + r0 < p.n) ? static_cast<int>(r0) : kRow;
     };
     // position of an offset inside the row, clamped to [0, 64] (memory safety
     // for malformed offsets; exact for valid ones)
@@ -1434,6 +1534,12 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
         long long i_lo = 0, i_hi = 0, i_tn = 1;  // i_tn: segment starts in the tile (uniform)
         long long i_k0 = 0, i_k1 = 0;            // the tile's starts: offsets [i_k0, i_k1)
         if constexpr (C::IRREG) i_tn = irreg_rows(t, par, i_lo, i_hi, i_k0, i_k1);
+        // SPLIT: the row's segment start (column sp_e, 64 = none); the raw 8
+        // elements of the granule it splits come from the tile's SMEM stage
+        // below (the stage is held until then)
+        int sp_e = 64;
+        uint4 sp_raw = make_uint4(0u, 0u, 0u, 0u);
+        if constexpr (MODE == MODE_SPLIT) sp_e = split_start(t, qmod);
         if (wait_full) ptx::mbar_wait_warp(&misc->tfull[a], aph);
         ptx::tc_fence_after();
         constexpr int LD = C::LD_COLS;
@@ -1453,6 +1559,31 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
         }
 
         const long long row = t * kTileRows + rit;
+        if constexpr (MODE == MODE_SPLIT) {
+          // the split granule's raw elements: one 16-B swizzled chunk of the
+          // row in the tile's SMEM stage (the MMA has consumed it: tfull),
+          // then the stage goes back to the producer (4 warp arrivals).  The
+          // ragged last row is outside the TMA view: read from HBM.
+          const int st = it % STAGES;
+          if (sp_e < kRow) {
+            if (row != p.rows_full) {
+              const uint32_t off16 = static_cast<uint32_t>(rit) * 128u +
+                                     ((static_cast<uint32_t>(sp_e >> 3) ^ static_cast<uint32_t>(rit & 7)) << 4);
+              sp_raw = *reinterpret_cast<const uint4*>(smem + st * kTileBytes + off16);
+            } else {
+              const long long gpos = row * kRow + (sp_e & ~7);
+              unsigned short hb[8];
+  #pragma unroll
+              for (int k = 0; k < 8; ++k)
+                hb[k] = (gpos + k < p.n) ? __ldg(reinterpret_cast<const unsigned short*>(p.x) + gpos + k)
+                                         : static_cast<unsigned short>(0);
+              sp_raw = *reinterpret_cast<const uint4*>(hb);
+            }
+          }
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&misc->empty[st]);
+        }
 
         if constexpr (C::IRREG && OP == OP_REDUCE) {
           // ================================================= irregular reduce
@@ -1797,6 +1928,20 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
               vv[k] = s;
             }
           }
+          // SPLIT: the raw elements of the split granule, and the total of
+          // its new part (columns k0..7: the new segment's first piece)
+          [[maybe_unused]] float sp_x[8];
+          [[maybe_unused]] float sp_tot = 0.f;
+          if constexpr (MODE == MODE_SPLIT) {
+            const uint32_t* hw = reinterpret_cast<const uint32_t*>(&sp_raw);
+  #pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const uint32_t b = (hw[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+              sp_x[k] = p.in_bf16 ? __uint_as_float(b << 16)
+                                  : __half2float(__ushort_as_half(static_cast<unsigned short>(b)));
+              if (k >= (sp_e & 7)) sp_tot += sp_x[k];
+            }
+          }
           // staging buffer reuse: the TMA store that last used this buffer
           // must have finished reading it before anyone writes (barrier below).
           if (leader) ptx::bulk_wait_read<C::OUT_BUFS - 1>();
@@ -1953,7 +2098,26 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
             int chain[GR];
             float run = 0.f;
             int seen = 0;
-            {
+            if constexpr (MODE == MODE_SPLIT) {
+              // granules of 8: before the split granule ge the open segment
+              // continues (chained), the granule's columns from k0 on start
+              // the new segment (their values come from the raw elements,
+              // below), and the later granules continue it from the
+              // new part's total.  Every value is a forward fp32 sum of its
+              // own segment's elements.
+              const int ge = sp_e >> 3;
+  #pragma unroll
+              for (int j = 0; j < GR; ++j) {
+                off[j] = run;
+                chain[j] = !seen;
+                if (j == ge) {
+                  run = sp_tot;
+                  seen = 1;
+                } else {
+                  run += vv[j * G + G - 1];
+                }
+              }
+            } else {
               // segment starts inside the row (32-bit granule offsets): the first
               // at (m - q0 % m) % m, then every m; none past the input's end,
               // and granule 0 continues the caller's segment when carried in
@@ -2003,7 +2167,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
             }
             compose(wv, wf, ve, fe);
             double tprefix;
-            if constexpr (MODE == MODE_GENERAL) {
+            if constexpr (MODE == MODE_GENERAL || MODE == MODE_SPLIT) {
               tprefix = carry;
               carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
               qmod += p.step_mod;
@@ -2101,6 +2265,57 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
             for (int k = 0; k < 64; ++k) {
               const long long e = row * kRow + k;
               if (e < p.n) out[e] = cvt_out<OutT>(outv(k));
+            }
+          }
+          if constexpr (MODE == MODE_SPLIT) {
+            // the split granule, rewritten in place from its raw elements:
+            // columns < k0 continue the old segment from off[ge] (carry
+            // included), columns >= k0 restart -- forward fp32 sums of each
+            // segment's own elements, no per-column selects elsewhere
+            if (sp_e < kRow) {
+              const int ge = sp_e >> 3, k0 = sp_e & 7;
+              float ro = off[0];
+  #pragma unroll
+              for (int j = 1; j < GR; ++j)
+                if (j == ge) ro = off[j];
+              float rn = 0.f;
+              float gv[8];
+  #pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const bool nw = k >= k0;
+                if (excl) gv[k] = nw ? rn : ro;
+                if (nw)
+                  rn += sp_x[k];
+                else
+                  ro += sp_x[k];
+                if (!excl) gv[k] = nw ? rn : ro;
+              }
+              if constexpr (sizeof(OutT) == 2) {
+                uint4 w;
+                __half2 h0 = __floats2half2_rn(gv[0], gv[1]);
+                __half2 h1 = __floats2half2_rn(gv[2], gv[3]);
+                __half2 h2 = __floats2half2_rn(gv[4], gv[5]);
+                __half2 h3 = __floats2half2_rn(gv[6], gv[7]);
+                w.x = *reinterpret_cast<uint32_t*>(&h0);
+                w.y = *reinterpret_cast<uint32_t*>(&h1);
+                w.z = *reinterpret_cast<uint32_t*>(&h2);
+                w.w = *reinterpret_cast<uint32_t*>(&h3);
+                *reinterpret_cast<uint4*>(stg + rb + ((static_cast<uint32_t>(ge) ^ sw) << 4)) = w;
+              } else {
+                const uint32_t c0 = 2u * static_cast<uint32_t>(ge & 3);
+                uint8_t* hb = stg + (ge >> 2) * 16384 + rb;
+                *reinterpret_cast<float4*>(hb + ((c0 ^ sw) << 4)) = make_float4(gv[0], gv[1], gv[2], gv[3]);
+                *reinterpret_cast<float4*>(hb + (((c0 + 1) ^ sw) << 4)) =
+                    make_float4(gv[4], gv[5], gv[6], gv[7]);
+              }
+              if (row == p.rows_full) {
+                OutT* out = reinterpret_cast<OutT*>(p.out);
+  #pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                  const long long e = row * kRow + 8 * ge + k;
+                  if (e < p.n) out[e] = cvt_out<OutT>(gv[k]);
+                }
+              }
             }
           }
           ptx::fence_proxy_async_smem();
@@ -2905,11 +3120,16 @@ static int rowseg_k(long long s, long long n, int out_esize) {
 
 // Segments per row for the MODE_ROWSEG scan (0 = not applicable): rows of
 // L = k s <= 64 kRssMaxChunks elements, k a power of two times 8 / gcd(s, 8),
-// the fewest chunks per element.  Only for the segment sizes whose granule
-// scan is slow (gcd(s, 64) <= 4: 16+ granules per row).
-static int rowseg_scan_k(long long s, long long n) {
-  if (s < 2 || s >= n) return 0;
-  if (gcd_ll(s, 64) > 4) return 0;
+// the fewest chunks per element.  Only where it beats the granule scan
+// (measured on B200, 2^30 fp16, % of copy bandwidth): s < 64 (larger s run
+// as MODE_SPLIT), gcd(s, 64) <= 2 (gcd 4: GENERAL 88 % vs 61-83 %); with
+// fp32 output GENERAL wins for gcd 2 (88 vs 71-80 %) and for odd s > 9
+// (73 vs 67-71 %).
+static int rowseg_scan_k(long long s, long long n, int out_esize) {
+  if (s < 2 || s >= n || s >= kRow) return 0;
+  const long long g = gcd_ll(s, 64);
+  if (g > 2) return 0;
+  if (out_esize == 4 && (g == 2 || s > 9)) return 0;
   int best = 0;
   double best_cost = 0.0;
   for (long long k = 8 / gcd_ll(s, 8); k * s <= 64LL * kRssMaxChunks; k *= 2) {
@@ -2930,8 +3150,8 @@ static size_t ws_need(int op, long long n, long long seg) {
   size_t b = kWsLookback;
   if (op == TC_OP_SCAN)
     b += static_cast<size_t>(chunk_slots(n)) * 2 * sizeof(uint64_t) + 64;
-  if (op == TC_OP_BN_STATS)  // per-(n, c) shifted moments (S1, S2), cleared after use
-    b += 2 * sizeof(double) * static_cast<size_t>((n + seg - 1) / (seg > 0 ? seg : 1)) + 512;
+  if (op == TC_OP_BN_STATS)  // per-(n, c) shifted moments (S1, S2) + per-channel tickets, cleared after use
+    b += (2 * sizeof(double) + sizeof(unsigned)) * static_cast<size_t>((n + seg - 1) / (seg > 0 ? seg : 1)) + 512;
   return (b + 255) & ~size_t(255);
 }
 
@@ -3008,7 +3228,8 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
   // match the API.
   if (MODE != MODE_CHUNK) {
     per_sm = (MODE == MODE_GSCR) ? 2
-             : (MODE == MODE_GENERAL || MODE == MODE_IRREG) ? Cfg<OP, GR, MODE, OutT>::MINB
+             : (MODE == MODE_GENERAL || MODE == MODE_IRREG || MODE == MODE_SPLIT)
+                 ? Cfg<OP, GR, MODE, OutT>::MINB
              : ((OP == OP_REDUCE && MODE == MODE_ROWS && p0.log2m >= 4 && p0.log2m < 7) ||
                 (OP == OP_SCAN && MODE == MODE_LOCAL && sizeof(OutT) == 4))
                  ? 2
@@ -3251,6 +3472,9 @@ static LaunchFn pick(int gr, int mode) {
       if constexpr (OP == OP_SCAN) return pick_gr<OP, MODE_CHUNK, OutT>(gr);
       return nullptr;
     case MODE_IRREG: return gr == 1 ? &launch<OP, 1, MODE_IRREG, OutT> : nullptr;
+    case MODE_SPLIT:
+      if constexpr (OP == OP_SCAN) return gr == 8 ? &launch<OP, 8, MODE_SPLIT, OutT> : nullptr;
+      return nullptr;
     case MODE_GSCR:
       if constexpr (OP == OP_REDUCE) {
         switch (gr) {
@@ -3296,12 +3520,24 @@ static int common_checks(const void* x, long long n, long long seg, const void* 
 }
 
 // Segment geometry -> granules, carry mode and per-mode constants.
+static bool split_enabled() {
+  const char* e = getenv("TC_SPLIT");  // tuning / A-B switch
+  return !(e && e[0] == '0');
+}
+// largest segment whose range-entry carry a bounded scan recomputes (above:
+// CHUNK).  GR = 1 keeps 2^18 (its CHUNK kernel streams at copy speed); the
+// multi-granule CHUNK epilogue is slow, so those scans re-read up to 2^21.
+static long long prepass_max(int gr) {
+  if (const char* e = getenv("TC_PREPASS_MAX")) return atoll(e);  // tuning / A-B switch
+  return gr == 1 ? kScanPrepassMax : (1LL << 21);
+}
+
 static Params make_params(const void* x, long long n, long long seg, void* out, void* ws, int op,
-                          bool has_carry, int* gr_out, int* mode_out) {
+                          bool has_carry, int* gr_out, int* mode_out, bool allow_split = false) {
   if (seg > n) seg = n;  // one segment spanning everything: same result, smaller m
   Params p{};
   const long long g = gcd_ll(seg, kRow);
-  const int gr = static_cast<int>(kRow / g);
+  int gr = static_cast<int>(kRow / g);
   p.x = reinterpret_cast<const __half*>(x);
   p.out = out;
   p.n = n;
@@ -3330,8 +3566,18 @@ static Params make_params(const void* x, long long n, long long seg, void* out, 
   } else {
     mode = MODE_GENERAL;
   }
+  if (op == TC_OP_SCAN && mode == MODE_GENERAL && allow_split && !scan_carry && g <= 4 &&
+      seg >= kRow && seg <= prepass_max(gr) && split_enabled()) {
+    // at most one start per row, few factors of two: granules of 8 with the
+    // split granule recomputed from its raw elements (MODE_SPLIT)
+    mode = MODE_SPLIT;
+    gr = 8;
+    p.m = seg;  // element granularity for the start bookkeeping
+    p.step_div = kTileElems / seg;
+    p.step_mod = kTileElems % seg;
+  }
   if (op == TC_OP_SCAN && (mode == MODE_TILES || mode == MODE_GENERAL) &&
-      (seg > kScanPrepassMax || scan_carry))
+      (seg > prepass_max(gr) || scan_carry))
     mode = MODE_CHUNK;
   *gr_out = gr;
   *mode_out = mode;
@@ -3441,7 +3687,7 @@ int tc_seg_scan_ex(const void* x, int in_dtype, int64_t n, int64_t seg, void* ou
     return TC_BAD_CONFIG;
   }
   if (carry_in == nullptr && total_out == nullptr) {
-    if (const int k = rowseg_enabled() ? rowseg_scan_k(seg, n) : 0) {
+    if (const int k = rowseg_enabled() ? rowseg_scan_k(seg, n, out_dtype == TC_F16 ? 2 : 4) : 0) {
       // whole segments per TMA row (MODE_ROWSEG): no carries between rows
       RssParams rp{};
       rp.x = reinterpret_cast<const __half*>(x);
@@ -3460,7 +3706,8 @@ int tc_seg_scan_ex(const void* x, int in_dtype, int64_t n, int64_t seg, void* ou
     }
   }
   int gr = 0, mode = 0;
-  Params p = make_params(x, n, seg, out, ws, TC_OP_SCAN, carry_in != nullptr, &gr, &mode);
+  Params p = make_params(x, n, seg, out, ws, TC_OP_SCAN, carry_in != nullptr, &gr, &mode,
+                         carry_in == nullptr && total_out == nullptr);
   p.exclusive = exclusive ? 1 : 0;
   p.in_bf16 = (in_dtype == TC_BF16) ? 1 : 0;
   p.carry_in = carry_in;
@@ -3589,14 +3836,54 @@ int tc_bn_stats(const void* x, int in_dtype, int64_t N, int64_t C, int64_t HW, v
   const __half* xh = reinterpret_cast<const __half*>(x);
   const int bf = in_dtype == TC_BF16 ? 1 : 0;
   long long groups = N;
-  if (HW % 8 == 0 && HW >= kBnChanMin) {
-    // per-channel blocks over sample ranges: ~8 blocks per SM
-    long long splits = (8LL * di.sms + C - 1) / C;
+  const int V = (HW % 8 == 0) ? 8 : (HW % 4 == 0) ? 4 : (HW % 2 == 0) ? 2 : 1;
+  long long chan_min = kBnChanMin;
+  if (const char* e = getenv("TC_BN_CHAN_MIN")) chan_min = atoll(e);  // tuning / A-B switch
+  if (HW >= chan_min && N * (HW / V) < (1LL << 31)) {
+    // per-channel blocks over sample ranges, ~4 full waves of 8 blocks / SM
+    // (a partial second wave cost ~10 % at C = 256)
+    const long long wave = 8LL * di.sms;
+    long long splits = (4 * wave) / C;
+    if (splits < 1) splits = 1;
     if (splits > N) splits = N;
     if (splits > 65535) splits = 65535;
     groups = splits;
-    bn_chan_kernel<<<dim3(static_cast<unsigned>(C), static_cast<unsigned>(splits)), kBnThreads, 0,
-                     st>>>(xh, bf, N, C, HW, mom);
+    const FastDiv fd = make_fastdiv(static_cast<uint32_t>(HW / V));
+    const dim3 grid(static_cast<unsigned>(C), static_cast<unsigned>(splits));
+    // per-channel arrival tickets: the dedicated always-zero region for
+    // C <= kBnMaxTicketC; otherwise after the moments, where other ops'
+    // scratch (the CHUNK scan's epoch-tagged look-back words) may linger,
+    // so they are zeroed first, stream-ordered
+    unsigned* ticket = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ws) + kWsBnTickets);
+    if (C > kBnMaxTicketC) {
+      ticket = reinterpret_cast<unsigned*>(mom + N * C);
+      if (cudaMemsetAsync(ticket, 0, sizeof(unsigned) * static_cast<size_t>(C), st) != cudaSuccess) {
+        set_err("cudaMemsetAsync failed: %s%lld", cudaGetErrorString(cudaGetLastError()), 0);
+        return TC_CUDA_ERROR;
+      }
+    }
+    auto go = [&](auto out_tag) {
+      using OutT = decltype(out_tag);
+      OutT* mo = reinterpret_cast<OutT*>(mean);
+      OutT* vo = reinterpret_cast<OutT*>(var);
+      switch (V) {
+        case 8: bn_chan_kernel<8, OutT><<<grid, kBnThreads, 0, st>>>(xh, bf, N, C, HW, fd, mom, ticket, mo, vo); break;
+        case 4: bn_chan_kernel<4, OutT><<<grid, kBnThreads, 0, st>>>(xh, bf, N, C, HW, fd, mom, ticket, mo, vo); break;
+        case 2: bn_chan_kernel<2, OutT><<<grid, kBnThreads, 0, st>>>(xh, bf, N, C, HW, fd, mom, ticket, mo, vo); break;
+        default: bn_chan_kernel<1, OutT><<<grid, kBnThreads, 0, st>>>(xh, bf, N, C, HW, fd, mom, ticket, mo, vo); break;
+      }
+    };
+    if (out_dtype == TC_F32)
+      go(0.f);
+    else
+      go(0.0);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      set_err("kernel launch failed: %s%lld", cudaGetErrorString(e), 0);
+      return TC_CUDA_ERROR;
+    }
+    g_launches += 1;
+    return TC_OK;
   } else {
     const long long per_block = HW < kBnWarpMin ? kBnThreads : kBnThreads / 32;  // segments
     long long blocks = (nsegs + per_block - 1) / per_block;
@@ -3630,7 +3917,7 @@ int tc_plan_info(int op, int64_t n, int64_t seg, int out_dtype, int has_carry, i
     if (op == TC_OP_REDUCE)
       k = rowseg_k(seg, n, es);
     else if (!has_carry && !has_total)
-      k = rowseg_scan_k(seg, n);
+      k = rowseg_scan_k(seg, n, es);
   }
   if (k) {
     *mode = MODE_ROWSEG;
@@ -3639,7 +3926,8 @@ int tc_plan_info(int op, int64_t n, int64_t seg, int out_dtype, int has_carry, i
   }
   static char dummy[1024];
   int gr = 0, md = 0;
-  make_params(dummy, n, seg, dummy, dummy, op, op == TC_OP_SCAN && has_carry, &gr, &md);
+  make_params(dummy, n, seg, dummy, dummy, op, op == TC_OP_SCAN && has_carry, &gr, &md,
+              !has_carry && !has_total);
   *mode = md;
   *row_len = kRow;
   return TC_OK;

@@ -269,4 +269,12 @@ def test_plan_info_modes():
     assert D.plan_info("scan", n, n)[0] == "CHUNK"
     assert D.plan_info("scan", n, 4096, carry_in=True)[0] == "CHUNK"
     assert D.plan_info("scan", n, 17)[0] == "ROWSEG"
+    assert D.plan_info("scan", n, 17, torch.float32)[0] == "GENERAL"
+    assert D.plan_info("scan", n, 3, torch.float32)[0] == "ROWSEG"
     assert D.plan_info("scan", n, 17, total_out=True)[0] == "GENERAL"
+    assert D.plan_info("scan", n, 12)[0] == "GENERAL"
+    for s in (65, 66, 100, 300, 4097, 100001, 1000003):
+        assert D.plan_info("scan", n, s)[0] == "SPLIT", s
+    assert D.plan_info("scan", n, 300, total_out=True)[0] == "GENERAL"
+    assert D.plan_info("scan", n, 1000)[0] == "GENERAL"
+    assert D.plan_info("scan", n, (1 << 21) + 1)[0] == "CHUNK"

@@ -17,8 +17,11 @@ from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
 
+# per-channel streaming kernel by vector width (HW % 8 / 4 / 2 / odd, HW >= 48)
+# and the per-segment kernel (HW < 48)
 SHAPES = [(2, 3, 7, 7), (1, 1, 1), (5, 2), (8, 64, 56, 56), (32, 256, 14, 14), (3, 17, 1000),
-          (256, 64, 28, 28), (4, 8, 300, 7)]
+          (256, 64, 28, 28), (4, 8, 300, 7), (64, 96, 7, 7), (7, 5, 50), (3, 300, 62),
+          (1, 2, 4096)]
 
 
 def check(mean, var, x):
@@ -67,3 +70,25 @@ def test_bn_bf16_and_forward_matches_torch(cuda):
     xb = x.to(torch.bfloat16)
     mb, vb = ht.batch_norm_stats(xb)
     check(mb.cpu().numpy(), vb.cpu().numpy(), xb.float().cpu().numpy())
+
+
+def test_bn_repeatable_and_workspace_clean(cuda):
+    """Two calls give bit-identical statistics (fixed combine order whichever
+    block finishes last), and a later CHUNK scan on the same stream's
+    workspace is unaffected (the statistics kernels re-zero their scratch)."""
+    from paper_1811_09736_b200 import _device as D
+
+    g = torch.Generator(device=cuda)
+    g.manual_seed(5)
+    # a CHUNK scan first: its epoch-tagged look-back words stay in the workspace
+    xs0 = torch.randint(-4, 5, ((1 << 20) + 5,), device=cuda, generator=g).to(torch.float16)
+    assert torch.equal(D.seg_scan(xs0, xs0.numel(), torch.float32), torch.cumsum(xs0.double(), 0).float())
+    x = (torch.rand(64, 256, 28, 28, device=cuda, generator=g) * 3 - 1).to(torch.float16)
+    m1, v1 = D.bn_stats(x)
+    check(m1.cpu().numpy(), v1.cpu().numpy(), x.cpu().numpy())
+    m2, v2 = D.bn_stats(x)
+    assert torch.equal(m1, m2) and torch.equal(v1, v2)
+    xs = torch.randint(-4, 5, ((1 << 21) + 3,), device=cuda, generator=g).to(torch.float16)
+    got = D.seg_scan(xs, xs.numel(), torch.float32)
+    ref = torch.cumsum(xs.double(), 0).float()
+    assert torch.equal(got, ref)

@@ -61,16 +61,18 @@ def main():
     if "scan" in which:
         import os
 
-        for s in [3, 5, 7, 9, 12, 17, 20, 33, 48, 63, 65, 100, 300, 1000, 100001, (1 << 19) + 3, n]:
+        for s in [3, 5, 6, 7, 9, 10, 12, 17, 20, 33, 34, 48, 63, 65, 66, 100, 130, 300, 1000, 4097, 100000,
+                  100001, (1 << 19) + 3, (1 << 19) + 4, n]:
             for dt, o in ((torch.float16, 2), (torch.float32, 4)):
                 out = torch.empty(n, dtype=dt, device=dev)
                 res = []
+                ab = os.environ.get("PROBE_AB", "TC_ROWSEG")  # A/B switch of the scan rows
                 for rs in ("1", "0"):
-                    os.environ["TC_ROWSEG"] = rs
+                    os.environ[ab] = rs
                     ms = timeit(lambda: D.seg_scan(x, s, dt, out=out))
                     gbs = (2 + o) * n / ms / 1e6
-                    res.append(f"rowseg={rs} {ms:7.3f} ms {gbs:6.0f} GB/s {100 * gbs / PEAK:5.1f}%")
-                os.environ.pop("TC_ROWSEG")
+                    res.append(f"{ab}={rs} {ms:7.3f} ms {gbs:6.0f} GB/s {100 * gbs / PEAK:5.1f}%")
+                os.environ.pop(ab)
                 print(f"scan   s={s:>10} {str(dt):14} " + " | ".join(res), flush=True)
     if "bn" in which:
         for shape in ((256, 256, 56, 56), (256, 512, 28, 28), (256, 1024, 14, 14),
@@ -78,7 +80,16 @@ def main():
             xb = torch.rand(shape, device=dev).to(torch.float16)
             ms = timeit(lambda: D.bn_stats(xb))
             gbs = 2 * xb.numel() / ms / 1e6
-            print(f"bn {shape}: {ms:7.3f} ms {gbs:6.0f} GB/s {100 * gbs / PEAK:5.1f}%", flush=True)
+            # the same call replayed from a CUDA graph (no host overhead)
+            D.bn_stats(xb)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                D.bn_stats(xb)
+            msg = timeit(g.replay)
+            gbsg = 2 * xb.numel() / msg / 1e6
+            print(f"bn {shape}: {ms:7.3f} ms {gbs:6.0f} GB/s {100 * gbs / PEAK:5.1f}% | graph "
+                  f"{msg:7.3f} ms {gbsg:6.0f} GB/s {100 * gbsg / PEAK:5.1f}%", flush=True)
             del xb
 
 
