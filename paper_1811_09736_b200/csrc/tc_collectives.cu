@@ -150,6 +150,8 @@ struct Params {
   int exclusive;
   int need_fixup;  // reduce: segments may straddle CTA ranges
   const long long* offs;  // IRREG: nseg + 1 non-decreasing offsets, offs[0] = 0, offs[nseg] = n
+  long long* tk0;         // IRREG reduce: first start index per tile (T + 1 entries, workspace)
+  void* trec;             // IRREG reduce: per-tile carry records (workspace)
 };
 
 template <typename T>
@@ -846,7 +848,7 @@ __device__ __forceinline__ uint32_t fastdiv(uint32_t i, const FastDiv& f) {
   return (__umulhi(i, f.mul) + i) >> f.shr;
 }
 
-template <int V, typename OutT>
+template <int V, int U, typename OutT>
 __global__ void __launch_bounds__(kBnThreads) bn_chan_kernel(const __half* x, int in_bf16,
                                                              long long N, long long C,
                                                              long long HW, FastDiv fd,
@@ -905,13 +907,13 @@ __global__ void __launch_bounds__(kBnThreads) bn_chan_kernel(const __half* x, in
   constexpr uint32_t step = kBnThreads;
   uint32_t i = threadIdx.x;
   int it = 0;
-  for (; i + 3 * step < total; i += 4 * step) {
-    const VT a = ld(i), b = ld(i + step), cc = ld(i + 2 * step), d = ld(i + 3 * step);
-    acc(a, 0);
-    acc(b, 1);
-    acc(cc, 0);
-    acc(d, 1);
-    if (++it == 64 / V) {  // fp32 partials to fp64 every 128 elements per slot
+  for (; i + (U - 1) * step < total; i += U * step) {
+    VT w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) w[u] = ld(i + u * step);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc(w[u], u & 1);
+    if (++it == 256 / (V * U)) {  // fp32 partials to fp64 every 128 elements per slot
       flush();
       it = 0;
     }
@@ -3021,6 +3023,454 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// =====================================================================
+// Irregular (CSR) segmented reduce, tile-parallel epilogue.
+//
+// The MMA is the scan's X.U64 (in-row inclusive prefixes in TMEM), as in
+// MODE_IRREG; what changes is how the epilogue finds and closes segments:
+//
+//  * a small pre-pass (irreg_k0_kernel, one coalesced read of the offsets)
+//    writes k0[t] = lower_bound(offsets, 8192 t) for every tile, so each
+//    tile knows its start range [k0[t], k0[t+1]) without searching;
+//  * kIrNG independent epilogue GROUPS (4 warps each, one per TMEM lane
+//    quadrant) take the CTA's tiles round-robin, each with its own SMEM
+//    staging of the in-row prefixes, offsets and named barrier, so kIrNG
+//    tiles are in the epilogue at once (the single group's per-tile latency
+//    bounded the previous design at ~50 % of copy bandwidth);
+//  * nothing flows between tiles inside the epilogue: a tile writes the
+//    segments that start and end in it, plus a record (head = value before
+//    its first start, tail = value after its last start, or its total), and
+//    after the range one warp composes the records in tile order
+//    (a segmented pair scan) to close the segments that cross tiles.  The
+//    range-crossing segments use the deterministic last-CTA fixup of the
+//    regular reduce.
+//
+// Numerics are those of MODE_IRREG: a segment inside one row is
+// P(b) - P(a) of fp32 in-row prefixes, a longer one adds an fp64 prefix of
+// row totals; tile and range carries are fp64.  The pre-pass table and the
+// records are re-zeroed after use (the workspace region is shared with the
+// CHUNK scan's epoch-tagged look-back words).
+#ifndef TC_IR_NG
+#define TC_IR_NG 3
+#endif
+constexpr int kIrNG = TC_IR_NG;  // epilogue groups (build-time: 3 measured best with 4 stages)
+constexpr int kIrStages = 4;
+constexpr int kIrAcc = 8;       // TMEM slots (64 columns each)
+constexpr int kIrThreads = 64 + kIrNG * kEpiThreads;
+constexpr int kIrCap = 256;     // offsets staged in SMEM per tile (more: read from L2)
+constexpr uint32_t kIrOffB = kIrStages * kTileBytes;
+constexpr uint32_t kIrOffScr = kIrOffB + 64 * 128;
+constexpr int kIrRowF = 68;     // staging row stride in floats (conflict-free 16-B stores)
+constexpr uint32_t kIrScrBytes = kTileRows * kIrRowF * 4;
+constexpr uint32_t kIrOffMisc = kIrOffScr + kIrNG * kIrScrBytes;
+constexpr uint32_t kIrFinalBar = 1 + kIrNG;  // named barrier of all epilogue groups
+
+struct IrRec {  // one tile's carry record
+  double h;       // sum before the first start (closes segment seg0)
+  double v;       // sum after the last start, or the whole tile (f == 0)
+  long long seg0; // k0[t] - 1
+  long long f;    // the tile holds a start
+};
+struct IrMisc {
+  uint64_t full[kIrStages];
+  uint64_t empty[kIrStages];
+  uint64_t tfull[kIrAcc];
+  uint64_t tempty[kIrAcc];
+  uint32_t tmem_base;
+  int is_last;
+  float wsum[kIrNG][2][4];
+  double wtot[kIrNG][2][4];
+  double rex[kIrNG][kTileRows];  // exclusive fp64 prefix of row totals within the row's warp
+  long long so[kIrNG][kIrCap];
+};
+constexpr uint32_t kIrSmem = kIrOffMisc + sizeof(IrMisc) + 1024;
+#ifdef TC_IRREG_TRACE
+// phase timestamps of CTA 0's group leaders (debug builds: -DTC_IRREG_TRACE)
+__device__ long long g_irtrace[kIrNG][64][8];
+#define IR_TRACE(ph) \
+  if (cta == 0 && leader && it < 64) g_irtrace[g][it][ph] = clock64();
+#else
+#define IR_TRACE(ph)
+#endif
+
+__global__ void irreg_k0_kernel(const long long* __restrict__ offs, long long nseg, long long T,
+                                long long* __restrict__ k0) {
+  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k > nseg) return;
+  const long long o = __ldg(offs + k);
+  long long tlo = 0;
+  if (k > 0) {
+    const long long op = __ldg(offs + k - 1);
+    tlo = (op < 0 ? -1 : op / kTileElems) + 1;
+  }
+  long long thi = o < 0 ? -1 : o / kTileElems;
+  if (thi > T - 1) thi = T - 1;
+  for (long long t = tlo; t <= thi; ++t) k0[t] = k;
+  if (k == nseg) k0[T] = nseg + 1;
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(kIrThreads, 1)
+    irreg_reduce_kernel(const __grid_constant__ CUtensorMap tin, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  IrMisc* misc = reinterpret_cast<IrMisc*>(smem + kIrOffMisc);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long T = p.num_tiles;
+  const int Gc = gridDim.x;
+  const int cta = blockIdx.x;
+  const long long t_begin = T * cta / Gc, t_end = T * (cta + 1) / Gc;
+  const int ntl = static_cast<int>(t_end - t_begin);
+  IrRec* rec = reinterpret_cast<IrRec*>(p.trec);
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tin);
+    for (int s = 0; s < kIrStages; ++s) {
+      ptx::mbar_init(&misc->full[s], 1);
+      ptx::mbar_init(&misc->empty[s], 1);
+    }
+    for (int a = 0; a < kIrAcc; ++a) {
+      ptx::mbar_init(&misc->tfull[a], 1);
+      ptx::mbar_init(&misc->tempty[a], 4);  // lane 0 of the group's 4 warps
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc(&misc->tmem_base, 512);
+    ptx::tmem_relinquish();
+  }
+  build_b<OP_SCAN, 1, 64>(smem + kIrOffB, p.in_bf16 ? 0x3F80 : 0x3C00);
+  ptx::fence_proxy_async_smem();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = misc->tmem_base;
+
+  if (warp == 0) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      const uint64_t pol = ptx::policy_evict_first();
+      for (int i = 0; i < ntl; ++i) {
+        const int s = i % kIrStages;
+        ptx::mbar_wait(&misc->empty[s], ((i / kIrStages) & 1) ^ 1u);
+        ptx::mbar_arrive_expect_tx(&misc->full[s], kTileBytes);
+        ptx::tma_load_2d(&tin, smem + s * kTileBytes, &misc->full[s], 0,
+                         static_cast<int32_t>((t_begin + i) * kTileRows), pol);
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer: X.U64 per tile =================
+    if (lane == 0) {
+      const uint32_t idesc = ptx::idesc_f16_f32(128, 64) | (p.in_bf16 ? ((1u << 7) | (1u << 10)) : 0u);
+      const uint64_t bdesc = ptx::smem_desc_sw128(smem + kIrOffB);
+      for (int i = 0; i < ntl; ++i) {
+        const int s = i % kIrStages;
+        const int a = i % kIrAcc;
+        ptx::mbar_wait(&misc->tempty[a], ((i / kIrAcc) & 1) ^ 1u);
+        ptx::mbar_wait(&misc->full[s], (i / kIrStages) & 1);
+        ptx::tc_fence_after();
+        const uint64_t adesc = ptx::smem_desc_sw128(smem + s * kTileBytes);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          ptx::mma_f16_ss(tmem + a * 64, adesc + 2 * k, bdesc + 2 * k, idesc, k > 0 ? 1u : 0u);
+        ptx::mma_commit(&misc->empty[s]);
+        ptx::mma_commit(&misc->tfull[a]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ================= epilogue groups =================
+    const int g = (warp - 2) >> 2;
+    const int qd = warp & 3;           // TMEM lane quadrant
+    const int rit = qd * 32 + lane;    // row in tile
+    const int et = threadIdx.x - 64 - g * kEpiThreads;
+    const bool leader = (et == 0);
+    const uint32_t bar = 1 + g;
+    const uint32_t lane_base = static_cast<uint32_t>(qd * 32) << 16;
+    float* scr = reinterpret_cast<float*>(smem + kIrOffScr + g * kIrScrBytes);
+    long long* so = misc->so[g];
+    double* rex = misc->rex[g];
+    OutT* out = reinterpret_cast<OutT*>(p.out);
+    constexpr long long kNoStart = 1LL << 62;
+    const long long kmax = p.nseg + 1;
+    auto ldk0 = [&](int i) -> long long {  // k0 of local tile i (i <= ntl); clamped at use
+      return __ldg(p.tk0 + t_begin + i);
+    };
+    auto clampk = [&](long long v) -> long long { return v < 0 ? 0 : (v > kmax ? kmax : v); };
+    auto ldoff = [&](long long k, long long lim) -> long long {
+      return k < lim ? __ldg(p.offs + k) : kNoStart;
+    };
+    // pipeline: this tile's range and first offsets, the next tile's range
+    // (k0 only: its offsets are loaded one tile ahead)
+    int i = g;
+    long long kA = 0, kB = 0, o0 = kNoStart, o1 = kNoStart, nA = 0, nB = 0;
+    if (i < ntl) {
+      kA = clampk(ldk0(i));
+      kB = clampk(ldk0(i + 1));
+      if (kB < kA) kB = kA;
+      o0 = ldoff(kA + et, kB);
+      o1 = ldoff(kA + et + kEpiThreads, kB);
+      if (i + kIrNG < ntl) {
+        nA = ldk0(i + kIrNG);  // raw: clamped when used, a tile later (no wait here)
+        nB = ldk0(i + kIrNG + 1);
+      }
+    }
+    for (int it = 0; i < ntl; i += kIrNG, ++it) {
+      const long long t = t_begin + i;
+      // prefetch: the next tile's offsets, the tile after's range
+      long long n0 = kNoStart, n1 = kNoStart, mA = 0, mB = 0;
+      if (i + kIrNG < ntl) {
+        nA = clampk(nA);
+        nB = clampk(nB);
+        if (nB < nA) nB = nA;
+        n0 = ldoff(nA + et, nB);
+        n1 = ldoff(nA + et + kEpiThreads, nB);
+        if (i + 2 * kIrNG < ntl) {  // raw loads: clamped a tile later
+          mA = ldk0(i + 2 * kIrNG);
+          mB = ldk0(i + 2 * kIrNG + 1);
+        }
+      }
+      const int a = i % kIrAcc;
+      const int par = it & 1;
+      IR_TRACE(0)
+      ptx::mbar_wait_warp(&misc->tfull[a], static_cast<uint32_t>((i / kIrAcc) & 1));
+      ptx::tc_fence_after();
+      IR_TRACE(1)
+      uint32_t r[64];
+      {
+        uint32_t(&r0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[0]);
+        uint32_t(&r1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[32]);
+        ptx::tmem_ld_32x32b<32>(tmem + lane_base + a * 64, r0);
+        ptx::tmem_ld_32x32b<32>(tmem + lane_base + a * 64 + 32, r1);
+      }
+      ptx::tmem_wait_ld();
+      IR_TRACE(2)
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&misc->tempty[a]);
+      float vv[64];
+#pragma unroll
+      for (int k = 0; k < 64; ++k) vv[k] = __uint_as_float(r[k]);
+      const long long row = t * kTileRows + rit;
+      if (row == p.rows_full) {  // ragged last row: outside the TMA view, recompute from HBM
+        float s = 0.f;
+#pragma unroll
+        for (int k = 0; k < 64; ++k) {
+          const long long e = row * kRow + k;
+          s += (e < p.n) ? in_to_float(p.x, e, p.in_bf16 != 0) : 0.f;
+          vv[k] = s;
+        }
+      }
+      const long long starts = kB - kA;
+      if (starts == 0) {
+        // no start in the tile: its total continues the open segment
+        const float ws = warp_sum(vv[63]);
+        if (lane == 0) misc->wsum[g][par][qd] = ws;
+        ptx::named_bar_sync(bar, kEpiThreads);
+        if (leader) {
+          const float* w = misc->wsum[g][par];
+          IrRec q;
+          q.h = 0.0;
+          q.v = static_cast<double>((w[0] + w[1]) + (w[2] + w[3]));
+          q.seg0 = kA - 1;
+          q.f = 0;
+          rec[t] = q;
+        }
+      } else {
+        // stage the row prefixes, the row totals' fp64 prefix and the offsets
+        float* srow = scr + rit * kIrRowF;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          *reinterpret_cast<float4*>(srow + 4 * j) =
+              make_float4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]);
+        IR_TRACE(7)
+        const double tr = static_cast<double>(vv[63]);
+        double incl = tr;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const double u = __shfl_up_sync(kFull, incl, d);
+          if (lane >= d) incl += u;
+        }
+        rex[rit] = incl - tr;
+        if (lane == 31) misc->wtot[g][par][qd] = incl;
+        so[et] = o0;
+        so[et + kEpiThreads] = o1;
+        IR_TRACE(3)
+        ptx::named_bar_sync(bar, kEpiThreads);
+        IR_TRACE(4)
+        const double* wt = misc->wtot[g][par];
+        const double wo1 = wt[0], wo2 = wo1 + wt[1], wo3 = wo2 + wt[2], tot = wo3 + wt[3];
+        const long long tb = t * kTileElems;
+        auto tpos = [&](long long o) -> int {  // position in the tile, clamped to [0, 8192]
+          const long long q = o - tb;
+          return static_cast<int>(q < 0 ? 0 : (q > kTileElems ? kTileElems : q));
+        };
+        auto prow = [&](int q) -> float {  // in-row prefix before position q
+          const int c = q & 63;
+          return c ? scr[(q >> 6) * kIrRowF + c - 1] : 0.f;
+        };
+        auto rpre = [&](int rr) -> double {  // tile prefix of row totals before row rr (0..128)
+          const int w = rr >> 5;
+          const double wo = w == 0 ? 0.0 : w == 1 ? wo1 : w == 2 ? wo2 : w == 3 ? wo3 : tot;
+          return rr >= kTileRows ? tot : wo + rex[rr];
+        };
+        auto offk = [&](long long j) -> long long {  // offset kA + j
+          return j < kIrCap ? so[j] : __ldg(p.offs + kA + j);
+        };
+        // segments that start and end in the tile: same row -> P(b) - P(a) in
+        // fp32, else the fp64 tile prefix of row totals joins in
+        for (long long j = et; j + 1 < starts; j += kEpiThreads) {
+          const int qa = tpos(offk(j)), qb = tpos(offk(j + 1));
+          if ((qa >> 6) == (qb >> 6)) {
+            out[kA + j] = cvt_out<OutT>(prow(qb) - prow(qa));
+          } else {
+            const double v = (rpre(qb >> 6) - rpre(qa >> 6)) +
+                             (static_cast<double>(prow(qb)) - static_cast<double>(prow(qa)));
+            out[kA + j] = cvt_out_d<OutT>(v);
+          }
+        }
+        if (et == kEpiThreads / 2) {  // the record: off the segment-0 thread's path
+          const int qf = tpos(offk(0)), ql = tpos(offk(starts - 1));
+          IrRec q;
+          q.h = rpre(qf >> 6) + static_cast<double>(prow(qf));
+          q.v = tot - (rpre(ql >> 6) + static_cast<double>(prow(ql)));
+          q.seg0 = kA - 1;
+          q.f = 1;
+          rec[t] = q;
+        }
+        IR_TRACE(5)
+        ptx::named_bar_sync(bar, kEpiThreads);  // staging, offsets and rex are rewritten next tile
+        IR_TRACE(6)
+      }
+      kA = nA;
+      kB = nB;
+      o0 = n0;
+      o1 = n1;
+      nA = mA;
+      nB = mB;
+    }
+
+    // ---- compose the records in tile order: close the segments that cross
+    // tiles, and hand the range's first / last open segment to the fixup
+    ptx::named_bar_sync(kIrFinalBar, kIrNG * kEpiThreads);
+    const long long krange0 = ntl > 0 ? ldk0(0) : 0;
+    const long long kend = ntl > 0 ? ldk0(ntl) : 0;
+    if (warp == 2) {
+      double carry = 0.0;
+      long long hseg = -1;
+      double hval = 0.0;
+      for (int base = 0; base < ntl; base += 32) {
+        const int j = base + lane;
+        IrRec q{0.0, 0.0, -1, 0};
+        if (j < ntl) {
+          q.h = __ldcg(&rec[t_begin + j].h);
+          q.v = __ldcg(&rec[t_begin + j].v);
+          q.seg0 = __ldcg(&rec[t_begin + j].seg0);
+          q.f = __ldcg(&rec[t_begin + j].f);
+          rec[t_begin + j] = IrRec{0.0, 0.0, 0, 0};
+        }
+        // inclusive segmented pair scan of (v, f) over the lanes
+        double v = q.v;
+        int f = static_cast<int>(q.f);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const double pv = __shfl_up_sync(kFull, v, d);
+          const int pf = __shfl_up_sync(kFull, f, d);
+          if (lane >= d) {
+            if (!f) v = pv + v;
+            f |= pf;
+          }
+        }
+        double ve = __shfl_up_sync(kFull, v, 1);
+        int fe = __shfl_up_sync(kFull, f, 1);
+        const double cin = (lane == 0) ? carry : (fe ? ve : carry + ve);
+        if (j < ntl && q.f && q.seg0 >= 0) {
+          const double val = cin + q.h;
+          if (q.seg0 < krange0) {  // began in an earlier CTA's range: a partial
+            hseg = q.seg0;
+            hval = val;
+          } else {
+            out[q.seg0] = cvt_out_d<OutT>(val);
+          }
+        }
+        const double vl = __shfl_sync(kFull, v, 31);
+        const int fl = __shfl_sync(kFull, f, 31);
+        carry = fl ? vl : carry + vl;
+      }
+      // at most one lane saw the range's head segment
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const long long hs2 = __shfl_xor_sync(kFull, hseg, o);
+        const double hv2 = __shfl_xor_sync(kFull, hval, o);
+        if (hs2 >= 0) {
+          hseg = hs2;
+          hval = hv2;
+        }
+      }
+      if (lane == 0) {
+        Entry e0{hseg, hval};
+        // the range's last start (kend - 1) stays open (its end offset is in a
+        // later range); in the last range it is the end offset itself
+        Entry e1{(kend - 1 >= 0 && kend - 1 < p.nseg) ? kend - 1 : -1LL, carry};
+        p.entries[2 * cta] = e0;
+        p.entries[2 * cta + 1] = e1;
+        __threadfence();
+        const unsigned tk = atomicAdd(&p.hdr->ticket, 1u);
+        misc->is_last = (tk == static_cast<unsigned>(Gc - 1));
+      }
+    }
+    // re-zero this range's interior k0 entries (the boundaries are shared
+    // with the neighbouring ranges: the last CTA clears them)
+    const int ft = threadIdx.x - 64;
+    for (long long tt = t_begin + 1 + ft; tt < t_end; tt += kIrNG * kEpiThreads) p.tk0[tt] = 0;
+    ptx::named_bar_sync(kIrFinalBar, kIrNG * kEpiThreads);
+    if (misc->is_last) {
+      __threadfence();
+      // deterministic combine of the range partials in CTA order (as the
+      // regular reduce's fixup), staged through the idle input ring
+      Entry* se = reinterpret_cast<Entry*>(smem);
+      const int ne = 2 * Gc;
+      for (int k = ft; k < ne; k += kIrNG * kEpiThreads) {
+        Entry e;
+        e.seg = __ldcg(&p.entries[k].seg);
+        e.val = __ldcg(&p.entries[k].val);
+        se[k] = e;
+      }
+      for (int c = ft; c <= Gc; c += kIrNG * kEpiThreads)
+        p.tk0[c == Gc ? T : T * c / Gc] = 0;
+      ptx::named_bar_sync(kIrFinalBar, kIrNG * kEpiThreads);
+      for (int k = ft; k < ne; k += kIrNG * kEpiThreads) {
+        const long long sg = se[k].seg;
+        if (sg < 0) continue;
+        int pk = k - 1;
+        while (pk >= 0 && se[pk].seg < 0) --pk;
+        if (pk >= 0 && se[pk].seg == sg) continue;  // not the first entry of its run
+        double acc = 0.0;
+        for (int kk = k; kk < ne; ++kk) {
+          const long long s2 = se[kk].seg;
+          if (s2 < 0) continue;
+          if (s2 != sg) break;
+          acc += se[kk].val;
+        }
+        out[sg] = cvt_out_d<OutT>(acc);
+      }
+      if (ft == 0) {
+        p.hdr->epoch = (p.hdr->epoch + 1u) & 0x3FFFFFFFu;
+        p.hdr->ticket = 0u;
+        __threadfence();
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
 // =====================================================================
 // host side
 // =====================================================================
@@ -3146,8 +3596,16 @@ static int rowseg_scan_k(long long s, long long n, int out_esize) {
 // CHUNK arrays: units u = j*Gc + c < T + kMaxCtas, chunks j < T
 static long long chunk_slots(long long n) { return (n + kTileElems - 1) / kTileElems + kMaxCtas; }
 
+// IRREG reduce scratch after the look-back region start: the per-tile k0
+// table (T + 1 entries) and the per-tile carry records
+static size_t irreg_k0_bytes(long long n) {
+  const long long T = (n + kTileElems - 1) / kTileElems;
+  return ((static_cast<size_t>(T + 1) * sizeof(long long)) + 255) & ~size_t(255);
+}
 static size_t ws_need(int op, long long n, long long seg) {
   size_t b = kWsLookback;
+  if (op == TC_OP_REDUCE)  // (irregular segments; small next to the data: 40 B per 16-KB tile)
+    b += irreg_k0_bytes(n) + sizeof(IrRec) * static_cast<size_t>((n + kTileElems - 1) / kTileElems) + 256;
   if (op == TC_OP_SCAN)
     b += static_cast<size_t>(chunk_slots(n)) * 2 * sizeof(uint64_t) + 64;
   if (op == TC_OP_BN_STATS)  // per-(n, c) shifted moments (S1, S2) + per-channel tickets, cleared after use
@@ -3437,6 +3895,58 @@ static int launch_rowseg_scan(const RssParams& p0, void* ws, cudaStream_t st) {
     return TC_CUDA_ERROR;
   }
   ++g_launches;
+  return TC_OK;
+}
+
+
+template <typename OutT>
+static int launch_irreg2(const Params& p0, cudaStream_t st) {
+  auto kern = irreg_reduce_kernel<OutT>;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::atomic<uint64_t> attr_done{0};
+  const uint64_t dev_bit = 1ull << (dev & 63);
+  if (!(attr_done.load() & dev_bit)) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kIrSmem) !=
+        cudaSuccess) {
+      set_err("cudaFuncSetAttribute failed: %s%lld", cudaGetErrorString(cudaGetLastError()), 0);
+      return TC_CUDA_ERROR;
+    }
+    attr_done.fetch_or(dev_bit);
+  }
+  const DevInfo di = dev_info(dev);
+  if (!di.ok || di.major < 10) {
+    set_err("no sm_100 device (compute capability major %s%lld)", "", di.major);
+    return TC_NO_DEVICE;
+  }
+  Params p = p0;
+  char* wsb = reinterpret_cast<char*>(p.hdr);
+  p.tk0 = reinterpret_cast<long long*>(wsb + kWsLookback);
+  p.trec = wsb + kWsLookback + irreg_k0_bytes(p.n);
+  long long grid = di.sms;  // one CTA per SM: kIrNG epilogue groups each
+  if (grid > p.num_tiles) grid = p.num_tiles;
+  if (grid > kMaxCtas) grid = kMaxCtas;
+  if (grid < 1) grid = 1;
+  CUtensorMap tin;
+  const void* in_base = p.rows_full > 0 ? static_cast<const void*>(p.x)
+                                        : static_cast<const void*>(wsb + kWsZeroRow);
+  if (!make_map(&tin, p.in_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                2, in_base, p.rows_full > 0 ? p.rows_full : 1, kRow)) {
+    set_err("cuTensorMapEncodeTiled (input) failed%s%lld", "", 0);
+    return TC_CUDA_ERROR;
+  }
+  const long long nk = p.nseg + 1;
+  irreg_k0_kernel<<<static_cast<unsigned>((nk + 255) / 256), 256, 0, st>>>(p.offs, p.nseg,
+                                                                          p.num_tiles, p.tk0);
+  kern<<<static_cast<unsigned>(grid), kIrThreads, kIrSmem, st>>>(tin, p);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_err("kernel launch failed: %s%lld", cudaGetErrorString(e), 0);
+    return TC_CUDA_ERROR;
+  }
+  g_launches += 2;
   return TC_OK;
 }
 
@@ -3774,6 +4284,13 @@ int tc_irreg_reduce(const void* x, int in_dtype, int64_t n, const int64_t* offse
   int rc = irreg_checks(x, in_dtype, n, offsets, nseg, out, out_dtype, false, ws, ws_bytes);
   if (rc) return rc;
   Params p = irreg_params(x, in_dtype, n, offsets, nseg, out, ws, TC_OP_REDUCE);
+  const char* v1 = getenv("TC_IRREG_V1");  // A/B switch: the single-group MODE_IRREG kernel
+  if (!(v1 && v1[0] == '1')) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    return out_dtype == TC_F16   ? launch_irreg2<__half>(p, st)
+           : out_dtype == TC_F32 ? launch_irreg2<float>(p, st)
+                                 : launch_irreg2<double>(p, st);
+  }
   LaunchFn fn = (out_dtype == TC_F16)   ? pick<OP_REDUCE, __half>(1, MODE_IRREG)
                 : (out_dtype == TC_F32) ? pick<OP_REDUCE, float>(1, MODE_IRREG)
                                         : pick<OP_REDUCE, double>(1, MODE_IRREG);
@@ -3843,7 +4360,11 @@ int tc_bn_stats(const void* x, int in_dtype, int64_t N, int64_t C, int64_t HW, v
     // per-channel blocks over sample ranges, ~4 full waves of 8 blocks / SM
     // (a partial second wave cost ~10 % at C = 256)
     const long long wave = 8LL * di.sms;
-    long long splits = (4 * wave) / C;
+    long long waves = 4;
+    int bn_unroll = 4;
+    if (const char* e = getenv("TC_BN_WAVES")) waves = atoll(e);  // tuning / A-B switches
+    if (const char* e = getenv("TC_BN_UNROLL")) bn_unroll = atoi(e);
+    long long splits = (waves * wave) / C;
     if (splits < 1) splits = 1;
     if (splits > N) splits = N;
     if (splits > 65535) splits = 65535;
@@ -3866,12 +4387,19 @@ int tc_bn_stats(const void* x, int in_dtype, int64_t N, int64_t C, int64_t HW, v
       using OutT = decltype(out_tag);
       OutT* mo = reinterpret_cast<OutT*>(mean);
       OutT* vo = reinterpret_cast<OutT*>(var);
-      switch (V) {
-        case 8: bn_chan_kernel<8, OutT><<<grid, kBnThreads, 0, st>>>(xh, bf, N, C, HW, fd, mom, ticket, mo, vo); break;
-        case 4: bn_chan_kernel<4, OutT><<<grid, kBnThreads, 0, st>>>(xh, bf, N, C, HW, fd, mom, ticket, mo, vo); break;
-        case 2: bn_chan_kernel<2, OutT><<<grid, kBnThreads, 0, st>>>(xh, bf, N, C, HW, fd, mom, ticket, mo, vo); break;
-        default: bn_chan_kernel<1, OutT><<<grid, kBnThreads, 0, st>>>(xh, bf, N, C, HW, fd, mom, ticket, mo, vo); break;
-      }
+      auto launch_v = [&](auto u_tag) {
+        constexpr int U = decltype(u_tag)::value;
+        switch (V) {
+          case 8: bn_chan_kernel<8, U, OutT><<<grid, kBnThreads, 0, st>>>(xh, bf, N, C, HW, fd, mom, ticket, mo, vo); break;
+          case 4: bn_chan_kernel<4, U, OutT><<<grid, kBnThreads, 0, st>>>(xh, bf, N, C, HW, fd, mom, ticket, mo, vo); break;
+          case 2: bn_chan_kernel<2, U, OutT><<<grid, kBnThreads, 0, st>>>(xh, bf, N, C, HW, fd, mom, ticket, mo, vo); break;
+          default: bn_chan_kernel<1, U, OutT><<<grid, kBnThreads, 0, st>>>(xh, bf, N, C, HW, fd, mom, ticket, mo, vo); break;
+        }
+      };
+      if (bn_unroll == 8)
+        launch_v(std::integral_constant<int, 8>{});
+      else
+        launch_v(std::integral_constant<int, 4>{});
     };
     if (out_dtype == TC_F32)
       go(0.f);
@@ -3950,6 +4478,12 @@ const char* tc_last_error(void) { return g_err; }
 
 uint64_t tc_launch_count(void) { return g_launches; }
 void tc_reset_launch_count(void) { g_launches = 0; }
+
+#ifdef TC_IRREG_TRACE
+int tc_debug_irreg_trace(void* host_out) {
+  return cudaMemcpyFromSymbol(host_out, g_irtrace, sizeof(g_irtrace)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 int tc_abi_version(void) { return (1 << 16) | 4; }
 
