@@ -158,20 +158,34 @@ int tc_irreg_scan(const void* x, int in_dtype, int64_t n, const int64_t* offsets
  * moments sum(x - K_c), sum((x - K_c)^2), K_c = x[0][c][0], then a fixed-
  * order fp64 combine per channel (CUDA cores: the squares need the elements,
  * which a constant-B MMA cannot give).  ws >= tc_workspace_bytes(
- * TC_OP_BN_STATS, N*C*HW, HW); the scratch is cleared again by the second
- * launch.  Two launches, stream-ordered. */
+ * TC_OP_BN_STATS, N*C*HW, HW); the scratch is cleared again after use.
+ * launch.  One launch (the channel's last block combines in split order;
+ * HW < 48: a per-segment kernel + a combine kernel), stream-ordered. */
 int tc_bn_stats(const void* x, int in_dtype, int64_t N, int64_t C, int64_t HW, void* mean,
                 void* var, int out_dtype, void* ws, size_t ws_bytes, void* stream);
 
 /* Diagnostics: which kernel a tc_seg_reduce / tc_seg_scan call with these
  * arguments runs.  *mode: 0 LOCAL, 1 ROWS, 2 TILES, 3 GENERAL, 4 CHUNK,
- * 5 IRREG, 6 GSCR, 7 ROWSEG (whole segments per TMA row).  *row_len: the
+ * 5 IRREG, 6 GSCR, 7 ROWSEG (whole segments per TMA row), 8 SPLIT (scan:
+ * granules of 8 with the one granule a segment start splits re-summed).  *row_len: the
  * elements of one MMA row -- 64, or k * seg for ROWSEG (rows of k whole
  * segments).  A non-finite input poisons the outputs computed from its MMA
  * row accumulation: the 64-element row, the whole ROWSEG row for a reduce,
  * the 64-column chunk of the ROWSEG row for a scan. */
 int tc_plan_info(int op, int64_t n, int64_t seg, int out_dtype, int has_carry, int has_total,
                  int* mode, int64_t* row_len);
+
+/* Host <-> device copies of PAGEABLE host memory (the drop-in's numpy
+ * arrays), staged through a pinned ring by a pool of host threads
+ * (non-temporal stores) overlapped with the copy engine.
+ * tc_h2d_pageable: stream-ordered on `stream`; returns once `src_host` may
+ * be reused (every byte is in pinned memory or already on the device).
+ * tc_d2h_pageable: ordered after earlier work on `stream`; returns when
+ * `dst_host` holds the data.  One transfer at a time per process (calls
+ * serialize).  Replaces the numpy <-> device conversion the reference does
+ * not need (its arrays never leave the host: reduce.py:69-73). */
+int tc_h2d_pageable(void* dst_dev, const void* src_host, size_t bytes, void* stream);
+int tc_d2h_pageable(void* dst_host, const void* src_dev, size_t bytes, void* stream);
 
 /* Human-readable name of a status code. */
 const char* tc_status_string(int status);
@@ -185,7 +199,8 @@ uint64_t tc_launch_count(void);
 void tc_reset_launch_count(void);
 
 /* ABI version: (major << 16) | minor.  1.1 added the *_ex entry points,
- * 1.2 the tc_irreg_* entry points, 1.3 tc_bn_stats, 1.4 tc_plan_info. */
+ * 1.2 the tc_irreg_* entry points, 1.3 tc_bn_stats, 1.4 tc_plan_info,
+ * 1.5 tc_h2d_pageable / tc_d2h_pageable. */
 int tc_abi_version(void);
 
 #ifdef __cplusplus

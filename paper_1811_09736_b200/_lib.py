@@ -60,6 +60,8 @@ SIGNATURES = {
                                    ctypes.c_int, _c_void_p, _size, _c_void_p]),
     "tc_plan_info": (ctypes.c_int, [ctypes.c_int, _i64, _i64, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_int, _c_void_p, _c_void_p]),
+    "tc_h2d_pageable": (ctypes.c_int, [_c_void_p, _c_void_p, _size, _c_void_p]),
+    "tc_d2h_pageable": (ctypes.c_int, [_c_void_p, _c_void_p, _size, _c_void_p]),
     "tc_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "tc_last_error": (ctypes.c_char_p, []),
     "tc_launch_count": (ctypes.c_uint64, []),
