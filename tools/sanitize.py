@@ -56,13 +56,18 @@ def run_reduce(x, xd, n, done):
 
 
 def run_scan(x, xd, n, done):
-    # scan: LOCAL, ROWS, TILES, GENERAL, CHUNK (s > 2^18 and full), carry-in
-    for s in (16, 256, 16384, 300, 48, 3):
+    # scan: LOCAL, ROWS, TILES, GENERAL (48, 1000), SPLIT (300, 65, 4097: the
+    # epilogue-held SMEM stage), ROWSEG (3; 17 with fp16 out)
+    for s in (16, 256, 16384, 300, 48, 3, 1000, 65, 4097):
         for exc in (False, True):
             got = D.seg_scan(xd, s, torch.float32, exclusive=exc).cpu().numpy()
             exp = O.ref_seg_scan(x, s, inclusive=not exc).astype(np.float32)
             assert np.array_equal(got, exp), ("scan", s, exc)
         done.append(f"scan s={s}")
+    for s in (17, 65):
+        got = D.seg_scan(xd, s, torch.float16).cpu().numpy()
+        assert np.array_equal(got, O.ref_seg_scan(x, s).astype(np.float16)), ("scan f16", s)
+        done.append(f"scan s={s} fp16")
 
 
 def run_chunk(x, xd, n, dev, done):
@@ -95,13 +100,15 @@ def run_irreg(x, xd, n, rng, dev, done):
 
 
 def run_bn(rng, dev, done):
-    # batch-norm statistics (HW = 49: the odd-segment path)
-    xb = rng.integers(-4, 5, (4, 8, 7, 7)).astype(np.float16)
-    m, v = D.bn_stats(torch.from_numpy(xb).to(dev), torch.float64)
-    em, ev = O.ref_bn_stats(xb)
-    assert np.allclose(m.cpu().numpy(), em, rtol=1e-12, atol=1e-12), "bn mean"
-    assert np.allclose(v.cpu().numpy(), ev, rtol=1e-9, atol=1e-9), "bn var"
-    done.append("batch-norm stats")
+    # batch-norm statistics: per-channel kernel (HW 49: 2-B vectors, HW 64:
+    # 16-B vectors, last-block combine) and the per-segment kernel (HW 25)
+    for shape in ((4, 8, 7, 7), (6, 8, 8, 8), (4, 8, 5, 5)):
+        xb = rng.integers(-4, 5, shape).astype(np.float16)
+        m, v = D.bn_stats(torch.from_numpy(xb).to(dev), torch.float64)
+        em, ev = O.ref_bn_stats(xb)
+        assert np.allclose(m.cpu().numpy(), em, rtol=1e-12, atol=1e-12), ("bn mean", shape)
+        assert np.allclose(v.cpu().numpy(), ev, rtol=1e-9, atol=1e-9), ("bn var", shape)
+        done.append(f"batch-norm stats {shape}")
 
 
 if __name__ == "__main__":
