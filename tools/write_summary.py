@@ -11,11 +11,14 @@ D = f"profiles/{rnd}"
 d = json.load(open(f"{D}/bench.json"))
 r = json.load(open(f"{D}/bench_ref.json"))
 ex = d["extras"]
-L = [f"# Round 1 profile summary (session {tag}, one B200)\n"]
-L.append(f"All numbers below come from `bench.json` / `bench_ref.json` / `ncu_*.txt` / `launches_summary.md` in this directory (one gpurun session, final round-1 code; `pytest_gpu.log`: {passed} GPU tests passed, `smoke.log` ok). Peak = measured copy bandwidth {d['roofline']['peak']:.1f} GB/s (`MEASURED_PEAKS.json`); read-dominated kernels can exceed it (a pure read stream is not bounded by the copy figure).\n")
+L = [f"# Round {rnd.lstrip('r').lstrip('0')} profile summary (session {tag}, one B200)\n"]
+L.append(f"All numbers below come from `bench.json` / `bench_ref.json` / `ncu_*.txt` / `launches_summary.md` in this directory (one gpurun session, this round's code; `pytest_gpu.log`: {passed} GPU tests passed, `smoke.log` ok). Peak = measured copy bandwidth {d['roofline']['peak']:.1f} GB/s (`MEASURED_PEAKS.json`); read-dominated kernels can exceed it (a pure read stream is not bounded by the copy figure).\n")
 L.append("## Headline (BASELINE configs[1]: segmented reduce, 2^30 fp16, s = 16..65536)\n")
 L.append(f"* value: {d['value']/1e9:.0f} Gelem/s device-resident ({d['ms_per_step']:.2f} ms per 13-launch sweep); roofline {d['roofline']['achieved']} GB/s = {100*d['roofline']['frac']:.1f} % of measured copy; DRAM traffic per launch {d['roofline']['traffic']/1e9:.3f} GB vs algorithmic 2.147-2.281 GB.")
 L.append(f"* e2e (pinned host -> chunked H2D -> public API -> D2H): {d['e2e']['value']/1e9:.0f} Gelem/s ({d['e2e']['ms_per_step']} ms/step, PCIe-bound: 2 GiB H2D per step).")
+pc = d.get("e2e_per_call")
+if pc:
+    L.append(f"* e2e per call (numpy in -> numpy out, one public call per size, each copying its own 2 GiB pageable input through the native stager): {pc['ms_per_call']} ms per call = {100*pc['frac_of_h2d_bound']:.0f} % of the pinned-H2D bound ({pc['pinned_h2d_gbs']} GB/s).")
 L.append(f"* reference arm (oracle/oracle.c, {r['cpu_baseline']['cores']} host threads): {r['value']/1e9:.1f} Gelem/s -> e2e / reference = {d['e2e']['value']/r['value']:.1f}x; device / reference = {d['value']/r['value']:.0f}x.")
 L.append(f"* clocks during the timed region: {d['clocks']}.\n")
 L.append("| s | ms | Gelem/s | GB/s | % of copy |\n|---|---|---|---|---|")
@@ -35,7 +38,9 @@ for row in ex["non_pow2_segments"]["rows"]:
 for row in ex["irregular_segments"]["rows"]:
     L.append(f"| irregular (CSR) mean {row['mean_seg']} ({row['nseg']} segs) reduce / scan, fp32 out | {row['reduce_ms']} / {row['scan_ms']} | | {100*row['reduce_frac']:.1f} / {100*row['scan_frac']:.1f} |")
 bn = ex["batch_norm_stats"]
-L.append(f"| batch-norm stats NCHW (256,256,56,56) | {bn['ms']} | {bn['gbs_algorithmic']} alg. / {bn['gbs_actual']} actual | {100*bn['frac_algorithmic']:.1f} (alg., 1 read) |")
+L.append(f"| batch-norm stats NCHW (256,256,56,56) | {bn['ms']} (graph {bn.get('ms_graph')}) | {bn['gbs_algorithmic']} | {100*bn['frac_algorithmic']:.1f} (one read) |")
+for row in ex.get("scan_sweep_f32", {}).get("rows", []):
+    L.append(f"| seg scan fp16->fp32 2^30, s={row['seg']} | {row['ms']} | {row['gbs_per_gpu']} | {100*row['frac']:.1f} |")
 L.append("\n## ncu --set full captures (2^30 inputs unless noted)\n")
 L.append("| capture | duration | DRAM read | DRAM write | regs | grid |\n|---|---|---|---|---|---|")
 for f in sorted(glob.glob(f"{D}/ncu_*.txt")):
