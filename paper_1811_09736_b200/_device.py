@@ -216,7 +216,7 @@ def bn_stats(x: torch.Tensor, out_dtype=torch.float32):
     return mean, var
 
 
-MODES = ("LOCAL", "ROWS", "TILES", "GENERAL", "CHUNK", "IRREG", "GSCR", "ROWSEG", "SPLIT")
+MODES = ("LOCAL", "ROWS", "TILES", "GENERAL", "CHUNK", "IRREG", "GSCR", "ROWSEG", "SPLIT", "SPLITM")
 
 
 def plan_info(op: str, n: int, seg: int, out_dtype=torch.float16, carry_in: bool = False,

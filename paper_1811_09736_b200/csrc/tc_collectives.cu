@@ -99,6 +99,9 @@ constexpr int MODE_ROWSEG = 7;  // whole segments per TMA row (rowseg_*_kernel)
 // (seg >= 64, gcd(seg, 64) <= 4): granules of 8 (GR = 8) with the one
 // granule that a start splits recomputed from its raw elements
 constexpr int MODE_SPLIT = 8;
+// the same for 9 <= seg < 64 (several starts per row, at most one per
+// granule of 8): every split granule re-summed from its raw elements
+constexpr int MODE_SPLITM = 9;
 constexpr int MODE_GSCR = 6;   // GENERAL reduce with many segment ends per row (2m < GR):
                                // end values staged in SMEM, interior segments stored coalesced
 constexpr int kMaxCtas = 1024;                    // persistent grid cap
@@ -207,7 +210,7 @@ struct Cfg {
   // buffer or 2 + 2.  The pair-scan modes (GENERAL, IRREG) prefer 2 + 2
   // (measured: s = 300 79 -> 87 % of copy bandwidth), the others 4 + 1.
   static constexpr bool SCAN32_2BUF =
-      (MODE == MODE_GENERAL || MODE == MODE_IRREG || MODE == MODE_SPLIT);
+      (MODE == MODE_GENERAL || MODE == MODE_IRREG || MODE == MODE_SPLIT || MODE == MODE_SPLITM);
   static constexpr int STAGES = CHUNK ? 8
                                 : (OP == OP_REDUCE)
                                     ? ((MINB == 3 || MODE == MODE_GSCR || MODE == MODE_IRREG) ? 4
@@ -1060,7 +1063,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
     if (OP == OP_SCAN) ptx::prefetch_tmap(&tout);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&misc->full[s], 1);
-      ptx::mbar_init(&misc->empty[s], MODE == MODE_SPLIT ? 4 : 1);  // SPLIT: the 4 epilogue warps
+      ptx::mbar_init(&misc->empty[s], (MODE == MODE_SPLIT || MODE == MODE_SPLITM) ? 4 : 1);  // SPLIT: the 4 epilogue warps
     }
     for (int a = 0; a < ACC; ++a) {
       ptx::mbar_init(&misc->tfull[a], 1);
@@ -1120,7 +1123,8 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
 #pragma unroll
         for (int k = 0; k < 4; ++k)  // K = 64 = 4 x 16; +32 B per K step inside the SW128 atom
           ptx::mma_f16_ss(tmem + a * N, adesc + 2 * k, bdesc + 2 * k, idesc, k > 0 ? 1u : 0u);
-        if constexpr (MODE != MODE_SPLIT) ptx::mma_commit(&misc->empty[s]);  // SPLIT: the epilogue frees it
+        if constexpr (MODE != MODE_SPLIT && MODE != MODE_SPLITM)
+          ptx::mma_commit(&misc->empty[s]);  // SPLIT: the epilogue frees it
         ptx::mma_commit(&misc->tfull[a]);
       });
     }
@@ -1145,7 +1149,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
       qmod = q0 % p.m;
       qdiv = q0 / p.m;
     }
-    if constexpr (MODE == MODE_SPLIT) {  // element granularity: the row's first element mod seg
+    if constexpr (MODE == MODE_SPLIT || MODE == MODE_SPLITM) {  // element granularity: the row's first element mod seg
       const long long e0 = (t_begin * kTileRows + rit) * kRow;
       qmod = e0 % p.m;
       qdiv = e0 / p.m;
@@ -1155,7 +1159,8 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
       tseg = t_begin / p.ktiles;
     }
     if constexpr (OP == OP_SCAN &&
-                  (MODE == MODE_TILES || MODE == MODE_GENERAL || MODE == MODE_SPLIT)) {
+                  (MODE == MODE_TILES || MODE == MODE_GENERAL || MODE == MODE_SPLIT ||
+                   MODE == MODE_SPLITM)) {
       // carry entering this CTA's range: the (< seg) elements of the open
       // segment that precede the range, re-read from HBM (bounded by
       // kScanPrepassMax), plus the caller's carry for segment 0.
@@ -1542,6 +1547,18 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
         int sp_e = 64;
         uint4 sp_raw = make_uint4(0u, 0u, 0u, 0u);
         if constexpr (MODE == MODE_SPLIT) sp_e = split_start(t, qmod);
+        // SPLITM: bit j of sm_mask = granule j holds a segment start, at
+        // column 8 j + ((sm_k0 >> 4 j) & 15)
+        uint32_t sm_mask = 0, sm_k0 = 0;
+        if constexpr (MODE == MODE_SPLITM) {
+          const long long rowpos = (t * kTileRows + rit) * kRow;
+          const int s32 = static_cast<int>(p.m);
+          const long long lim = p.n - rowpos;
+          for (int e = qmod == 0 ? 0 : static_cast<int>(p.m - qmod); e < kRow && e < lim; e += s32) {
+            sm_mask |= 1u << (e >> 3);
+            sm_k0 |= static_cast<uint32_t>(e & 7) << (4 * (e >> 3));
+          }
+        }
         if (wait_full) ptx::mbar_wait_warp(&misc->tfull[a], aph);
         ptx::tc_fence_after();
         constexpr int LD = C::LD_COLS;
@@ -1561,6 +1578,31 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
         }
 
         const long long row = t * kTileRows + rit;
+        // SPLITM: granule j's 8 raw elements from the tile's SMEM stage (held
+        // until the outputs are staged), or from HBM for the ragged last row
+        [[maybe_unused]] auto raw8 = [&](int j, float (&xr)[8]) {
+          uint4 w;
+          if (row != p.rows_full) {
+            const uint32_t off16 = static_cast<uint32_t>(rit) * 128u +
+                                   ((static_cast<uint32_t>(j) ^ static_cast<uint32_t>(rit & 7)) << 4);
+            w = *reinterpret_cast<const uint4*>(smem + (it % STAGES) * kTileBytes + off16);
+          } else {
+            const long long gpos = row * kRow + 8 * j;
+            unsigned short hb[8];
+  #pragma unroll
+            for (int k = 0; k < 8; ++k)
+              hb[k] = (gpos + k < p.n) ? __ldg(reinterpret_cast<const unsigned short*>(p.x) + gpos + k)
+                                       : static_cast<unsigned short>(0);
+            w = *reinterpret_cast<const uint4*>(hb);
+          }
+          const uint32_t* hw = reinterpret_cast<const uint32_t*>(&w);
+  #pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t b = (hw[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+            xr[k] = p.in_bf16 ? __uint_as_float(b << 16)
+                              : __half2float(__ushort_as_half(static_cast<unsigned short>(b)));
+          }
+        };
         if constexpr (MODE == MODE_SPLIT) {
           // the split granule's raw elements: one 16-B swizzled chunk of the
           // row in the tile's SMEM stage (the MMA has consumed it: tfull),
@@ -1930,6 +1972,33 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
               vv[k] = s;
             }
           }
+          if constexpr (MODE == MODE_SPLITM) {
+            // every granule a segment start splits is re-summed from its raw
+            // elements (the tile's SMEM stage) as two restarted prefixes:
+            // columns < k0 from the granule start (the old segment), columns
+            // >= k0 from k0 (the new one); then the stage is released
+  #pragma unroll
+            for (int j = 0; j < GR; ++j) {
+              if (!((sm_mask >> j) & 1u)) continue;
+              const int k0 = static_cast<int>((sm_k0 >> (4 * j)) & 15u);
+              float xr[8];
+              raw8(j, xr);
+              float ao = 0.f, an = 0.f;
+  #pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                if (k < k0) {
+                  ao += xr[k];
+                  vv[j * G + k] = ao;
+                } else {
+                  an += xr[k];
+                  vv[j * G + k] = an;
+                }
+              }
+            }
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&misc->empty[it % STAGES]);
+          }
           // SPLIT: the raw elements of the split granule, and the total of
           // its new part (columns k0..7: the new segment's first piece)
           [[maybe_unused]] float sp_x[8];
@@ -2119,6 +2188,17 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
                   run += vv[j * G + G - 1];
                 }
               }
+            } else if constexpr (MODE == MODE_SPLITM) {
+              // split granules hold restarted prefixes (above): their last
+              // column is the new segment's first piece
+  #pragma unroll
+              for (int j = 0; j < GR; ++j) {
+                off[j] = run;
+                chain[j] = !seen;
+                const bool sp = (sm_mask >> j) & 1u;
+                run = sp ? vv[j * G + G - 1] : run + vv[j * G + G - 1];
+                seen |= sp ? 1 : 0;
+              }
             } else {
               // segment starts inside the row (32-bit granule offsets): the first
               // at (m - q0 % m) % m, then every m; none past the input's end,
@@ -2169,7 +2249,7 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
             }
             compose(wv, wf, ve, fe);
             double tprefix;
-            if constexpr (MODE == MODE_GENERAL || MODE == MODE_SPLIT) {
+            if constexpr (MODE == MODE_GENERAL || MODE == MODE_SPLIT || MODE == MODE_SPLITM) {
               tprefix = carry;
               carry = tf ? static_cast<double>(tv) : carry + static_cast<double>(tv);
               qmod += p.step_mod;
@@ -2216,6 +2296,14 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
           const bool excl = p.exclusive != 0;
           auto outv = [&](int e) -> float {
             if constexpr (C::IRREG) return vv[e];  // already final
+            if constexpr (MODE == MODE_SPLITM) {
+              // columns from the split point on restart (offset 0; exclusive: 0 at the start)
+              const int k = e & 7;
+              const int cut = ((sm_mask >> (e >> 3)) & 1u) ? static_cast<int>((sm_k0 >> (4 * (e >> 3))) & 15u) : 8;
+              const float base = (k >= cut) ? 0.f : off[e >> 3];
+              if (excl) return (k == 0 || k == cut) ? (base + 0.f) : (vv[e - 1] + base);
+              return vv[e] + base;
+            }
             const float base = off[ONE_OFF ? 0 : e / G];
             if (excl) return (e % G == 0) ? (base + 0.f) : (vv[e - 1] + base);
             return vv[e] + base;
@@ -3575,8 +3663,12 @@ static int rowseg_k(long long s, long long n, int out_esize) {
 // as MODE_SPLIT), gcd(s, 64) <= 2 (gcd 4: GENERAL 88 % vs 61-83 %); with
 // fp32 output GENERAL wins for gcd 2 (88 vs 71-80 %) and for odd s > 9
 // (73 vs 67-71 %).
+static bool split_enabled();
+static bool splitm_wins(long long s, int out_esize);
+constexpr long long kSplitMMin = 9;  // >= 9: at most one start per granule of 8
 static int rowseg_scan_k(long long s, long long n, int out_esize) {
   if (s < 2 || s >= n || s >= kRow) return 0;
+  if (split_enabled() && splitm_wins(s, out_esize)) return 0;  // MODE_SPLITM
   const long long g = gcd_ll(s, 64);
   if (g > 2) return 0;
   if (out_esize == 4 && (g == 2 || s > 9)) return 0;
@@ -3686,7 +3778,8 @@ static int launch(const Params& p0, int out_esize, cudaStream_t st) {
   // match the API.
   if (MODE != MODE_CHUNK) {
     per_sm = (MODE == MODE_GSCR) ? 2
-             : (MODE == MODE_GENERAL || MODE == MODE_IRREG || MODE == MODE_SPLIT)
+             : (MODE == MODE_GENERAL || MODE == MODE_IRREG || MODE == MODE_SPLIT ||
+                MODE == MODE_SPLITM)
                  ? Cfg<OP, GR, MODE, OutT>::MINB
              : ((OP == OP_REDUCE && MODE == MODE_ROWS && p0.log2m >= 4 && p0.log2m < 7) ||
                 (OP == OP_SCAN && MODE == MODE_LOCAL && sizeof(OutT) == 4))
@@ -3985,6 +4078,9 @@ static LaunchFn pick(int gr, int mode) {
     case MODE_SPLIT:
       if constexpr (OP == OP_SCAN) return gr == 8 ? &launch<OP, 8, MODE_SPLIT, OutT> : nullptr;
       return nullptr;
+    case MODE_SPLITM:
+      if constexpr (OP == OP_SCAN) return gr == 8 ? &launch<OP, 8, MODE_SPLITM, OutT> : nullptr;
+      return nullptr;
     case MODE_GSCR:
       if constexpr (OP == OP_REDUCE) {
         switch (gr) {
@@ -4034,6 +4130,17 @@ static bool split_enabled() {
   const char* e = getenv("TC_SPLIT");  // tuning / A-B switch
   return !(e && e[0] == '0');
 }
+static bool splitm_enabled() {
+  const char* e = getenv("TC_SPLITM");  // tuning / A-B switch
+  return !(e && e[0] == '0');
+}
+// MODE_SPLITM only where it measured faster (B200, 2^30, % of copy): fp32
+// output, odd s in [11, 64) (s = 17 / 33 / 63: 79 / 80 / 93 % vs GENERAL
+// 75 %); fp16 output keeps ROWSEG (SPLITM 44-52 %), gcd 2 / 4 keep GENERAL
+// (87 % vs 76-80 %)
+static bool splitm_wins(long long s, int out_esize) {
+  return splitm_enabled() && out_esize == 4 && (s & 1) && s >= 11 && s < kRow;
+}
 // largest segment whose range-entry carry a bounded scan recomputes (above:
 // CHUNK).  GR = 1 keeps 2^18 (its CHUNK kernel streams at copy speed); the
 // multi-granule CHUNK epilogue is slow, so those scans re-read up to 2^21.
@@ -4043,7 +4150,8 @@ static long long prepass_max(int gr) {
 }
 
 static Params make_params(const void* x, long long n, long long seg, void* out, void* ws, int op,
-                          bool has_carry, int* gr_out, int* mode_out, bool allow_split = false) {
+                          bool has_carry, int* gr_out, int* mode_out, bool allow_split = false,
+                          int out_esize = 2) {
   if (seg > n) seg = n;  // one segment spanning everything: same result, smaller m
   Params p{};
   const long long g = gcd_ll(seg, kRow);
@@ -4077,10 +4185,12 @@ static Params make_params(const void* x, long long n, long long seg, void* out, 
     mode = MODE_GENERAL;
   }
   if (op == TC_OP_SCAN && mode == MODE_GENERAL && allow_split && !scan_carry && g <= 4 &&
-      seg >= kRow && seg <= prepass_max(gr) && split_enabled()) {
-    // at most one start per row, few factors of two: granules of 8 with the
-    // split granule recomputed from its raw elements (MODE_SPLIT)
-    mode = MODE_SPLIT;
+      seg >= kSplitMMin && seg <= prepass_max(gr) && split_enabled() &&
+      (seg >= kRow || splitm_wins(seg, out_esize))) {
+    // few factors of two: granules of 8, each granule a segment start
+    // splits recomputed from its raw elements (one start per row: MODE_SPLIT;
+    // several: MODE_SPLITM)
+    mode = seg >= kRow ? MODE_SPLIT : MODE_SPLITM;
     gr = 8;
     p.m = seg;  // element granularity for the start bookkeeping
     p.step_div = kTileElems / seg;
@@ -4217,7 +4327,7 @@ int tc_seg_scan_ex(const void* x, int in_dtype, int64_t n, int64_t seg, void* ou
   }
   int gr = 0, mode = 0;
   Params p = make_params(x, n, seg, out, ws, TC_OP_SCAN, carry_in != nullptr, &gr, &mode,
-                         carry_in == nullptr && total_out == nullptr);
+                         carry_in == nullptr && total_out == nullptr, out_dtype == TC_F16 ? 2 : 4);
   p.exclusive = exclusive ? 1 : 0;
   p.in_bf16 = (in_dtype == TC_BF16) ? 1 : 0;
   p.carry_in = carry_in;
@@ -4456,7 +4566,7 @@ int tc_plan_info(int op, int64_t n, int64_t seg, int out_dtype, int has_carry, i
   static char dummy[1024];
   int gr = 0, md = 0;
   make_params(dummy, n, seg, dummy, dummy, op, op == TC_OP_SCAN && has_carry, &gr, &md,
-              !has_carry && !has_total);
+              !has_carry && !has_total, es);
   *mode = md;
   *row_len = kRow;
   return TC_OK;

@@ -269,7 +269,10 @@ def test_plan_info_modes():
     assert D.plan_info("scan", n, n)[0] == "CHUNK"
     assert D.plan_info("scan", n, 4096, carry_in=True)[0] == "CHUNK"
     assert D.plan_info("scan", n, 17)[0] == "ROWSEG"
-    assert D.plan_info("scan", n, 17, torch.float32)[0] == "GENERAL"
+    assert D.plan_info("scan", n, 17, torch.float32)[0] == "SPLITM"
+    assert D.plan_info("scan", n, 63, torch.float32)[0] == "SPLITM"
+    assert D.plan_info("scan", n, 34, torch.float32)[0] == "GENERAL"
+    assert D.plan_info("scan", n, 9, torch.float32)[0] == "ROWSEG"
     assert D.plan_info("scan", n, 3, torch.float32)[0] == "ROWSEG"
     assert D.plan_info("scan", n, 17, total_out=True)[0] == "GENERAL"
     assert D.plan_info("scan", n, 12)[0] == "GENERAL"

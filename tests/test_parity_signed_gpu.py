@@ -47,12 +47,13 @@ N = (1 << 22) + 1234  # ragged: not a multiple of 64, 8192 or any segment size
 #   per row: 3, 7, 17, 24, 63, 12, 20)
 REDUCE_SEGS = [1, 2, 16, 64, 256, 8192, 16384, 24576, 3, 7, 12, 17, 20, 24, 63, 48, 65, 100,
                300, 1000, 100001, N]
-#   scans: LOCAL / ROWS / TILES / GENERAL as above; ROWSEG (s < 64, gcd(s, 64)
-#   <= 2: 3, 6, 10, 17 with fp16 out); SPLIT (s >= 64, gcd(s, 64) <= 4, up to
+#   scans: LOCAL / ROWS / TILES / GENERAL as above; ROWSEG (s < 9, gcd(s, 64)
+#   <= 2, fp16 out: 3, 6, 9, 17, 33, 63; fp32 out s <= 9); SPLITM (fp32 out, odd
+#   11 <= s < 64: 17, 33, 63); SPLIT (s >= 64, gcd(s, 64) <= 4, up to
 #   2^21: 65, 66, 100, 130, 300, 4097, 100001, 524292, 1000003); CHUNK for
 #   s > 2^18 with one granule per row ((1 << 18) + 8192), s > 2^21 and full
-SCAN_SEGS = [1, 16, 64, 256, 8192, 16384, 3, 6, 10, 17, 48, 65, 66, 100, 130, 300, 1000, 4097,
-             100001, (1 << 18) + 8192, 524292, 1000003, (1 << 21) + 1, N]
+SCAN_SEGS = [1, 16, 64, 256, 8192, 16384, 3, 6, 9, 10, 12, 17, 33, 48, 63, 65, 66, 100, 130, 300,
+             1000, 4097, 100001, (1 << 18) + 8192, 524292, 1000003, (1 << 21) + 1, N]
 
 
 def _ulp(v, dt):

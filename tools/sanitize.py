@@ -57,8 +57,8 @@ def run_reduce(x, xd, n, done):
 
 def run_scan(x, xd, n, done):
     # scan: LOCAL, ROWS, TILES, GENERAL (48, 1000), SPLIT (300, 65, 4097: the
-    # epilogue-held SMEM stage), ROWSEG (3; 17 with fp16 out)
-    for s in (16, 256, 16384, 300, 48, 3, 1000, 65, 4097):
+    # epilogue-held SMEM stage), SPLITM (33, fp32 out), ROWSEG (3; 17 with fp16 out)
+    for s in (16, 256, 16384, 300, 48, 3, 1000, 65, 4097, 33):
         for exc in (False, True):
             got = D.seg_scan(xd, s, torch.float32, exclusive=exc).cpu().numpy()
             exp = O.ref_seg_scan(x, s, inclusive=not exc).astype(np.float32)
