@@ -57,7 +57,11 @@ _IN = {torch.float16: _lib.TC_F16, torch.bfloat16: _lib.TC_BF16}
 
 def _prep(x: torch.Tensor) -> torch.Tensor:
     """fp16 (the reference's input type) or bf16 (extension) stay as they
-    are; anything else is converted to fp16 like reduce._as_flat_half."""
+    are; anything else is converted to fp16 like reduce._as_flat_half.
+
+    A non-contiguous view, or one whose data pointer is not 16-byte aligned
+    (TMA rows need it, e.g. ``x[3:]``), costs ONE extra device copy here;
+    aligned contiguous fp16 / bf16 tensors are used in place."""
     if not x.is_cuda:
         raise ValueError("device entry points take CUDA tensors")
     if x.dim() != 1:
