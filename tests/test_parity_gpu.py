@@ -198,11 +198,14 @@ def test_bf16_input(n, cuda, rng):
     """bf16 input (tcgen05 kind::f16 with BF16 operands; extension beyond the
     fp16-only reference): bit-exact on small integers (exact in bf16 and in
     every partial sum), and within the fp32 tolerance on uniform data, across
-    the LOCAL / ROWS / TILES / GENERAL / CHUNK modes."""
+    the LOCAL / ROWS / TILES / GENERAL / SPLIT / SPLITM / ROWSEG / CHUNK modes
+    (SPLIT / SPLITM convert the raw bf16 elements of split granules too)."""
     xi = rng.integers(0, 8, n).astype(np.float32)
     xd = torch.from_numpy(xi).to(cuda).to(torch.bfloat16)
     x64 = xd.double().cpu().numpy()
-    for s in (16, 48, 256, 8192, 300, 1 << 19, n):
+    # modes: LOCAL 16, GENERAL 48, ROWS 256, TILES 8192, SPLIT 300 / 100001,
+    # SPLITM 33 (fp32 out), ROWSEG 3 / 17, CHUNK 2^19 and n
+    for s in (16, 48, 256, 8192, 300, 100001, 33, 17, 3, 1 << 19, n):
         got = D.seg_reduce(xd, s, torch.float32).cpu().numpy()
         assert np.array_equal(got, O.ref_seg_reduce(x64, s).astype(np.float32)), (n, s)
         for exc in (False, True):
