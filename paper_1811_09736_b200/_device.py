@@ -12,7 +12,7 @@ from __future__ import annotations
 import torch
 
 from . import _lib
-from .errors import BadConfigError, BadLengthError
+from .errors import STATUS_ERRORS, BadConfigError, BadLengthError
 
 _DT = {torch.float16: _lib.TC_F16, torch.float32: _lib.TC_F32, torch.float64: _lib.TC_F64}
 
@@ -23,10 +23,9 @@ def _check(rc: int) -> None:
     if rc == _lib.TC_OK:
         return
     msg = _lib.last_error()
-    if rc == _lib.TC_BAD_LENGTH:
-        raise BadLengthError(msg)
-    if rc == _lib.TC_BAD_CONFIG:
-        raise BadConfigError(msg)
+    exc = STATUS_ERRORS.get(rc)
+    if exc is not None:
+        raise exc(msg)
     raise RuntimeError(f"tc_collectives: {_lib.status_string(rc)}: {msg}")
 
 
