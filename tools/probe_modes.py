@@ -76,7 +76,7 @@ def main():
                 print(f"scan   s={s:>10} {str(dt):14} " + " | ".join(res), flush=True)
     if "bn" in which:
         for shape in ((256, 256, 56, 56), (256, 512, 28, 28), (256, 1024, 14, 14),
-                      (256, 2048, 7, 7)):
+                      (256, 2048, 7, 7), (64, 96, 35, 35), (32, 384, 17, 17)):
             xb = torch.rand(shape, device=dev).to(torch.float16)
             ms = timeit(lambda: D.bn_stats(xb))
             gbs = 2 * xb.numel() / ms / 1e6
