@@ -18,6 +18,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -223,8 +224,18 @@ class Stager {
   bool used_[kRing] = {};
 };
 
+// Process-lifetime singleton (never destroyed: no exit-order hazards).  A
+// fork()ed child inherits the object but not its pool threads, so the child
+// builds its own on first use.
 Stager& stager() {
-  static Stager* s = new Stager();  // process lifetime (never destroyed: no exit-order hazards)
+  static std::mutex mu;
+  static Stager* s = nullptr;
+  static pid_t owner = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  if (s == nullptr || owner != getpid()) {
+    s = new Stager();
+    owner = getpid();
+  }
   return *s;
 }
 
