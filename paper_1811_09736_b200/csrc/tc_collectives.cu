@@ -1985,14 +1985,11 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
               raw8(j, xr);
               float ao = 0.f, an = 0.f;
   #pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                if (k < k0) {
-                  ao += xr[k];
-                  vv[j * G + k] = ao;
-                } else {
-                  an += xr[k];
-                  vv[j * G + k] = an;
-                }
+              for (int k = 0; k < 8; ++k) {  // branch-free (a branch per column cost ~25 % of issue)
+                const bool nw = k >= k0;
+                ao = nw ? ao : ao + xr[k];
+                an = nw ? an + xr[k] : an;
+                vv[j * G + k] = nw ? an : ao;
               }
             }
             ptx::fence_proxy_async_smem();
@@ -2294,12 +2291,17 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
           // produced chunk by chunk straight into the swizzled staging tile.
           constexpr bool ONE_OFF = (MODE == MODE_ROWS || MODE == MODE_TILES);
           const bool excl = p.exclusive != 0;
+          [[maybe_unused]] int sm_cut[GR];  // SPLITM: restart column per granule (8: none)
+          if constexpr (MODE == MODE_SPLITM) {
+  #pragma unroll
+            for (int j = 0; j < GR; ++j)
+              sm_cut[j] = ((sm_mask >> j) & 1u) ? static_cast<int>((sm_k0 >> (4 * j)) & 15u) : 8;
+          }
           auto outv = [&](int e) -> float {
             if constexpr (C::IRREG) return vv[e];  // already final
             if constexpr (MODE == MODE_SPLITM) {
               // columns from the split point on restart (offset 0; exclusive: 0 at the start)
-              const int k = e & 7;
-              const int cut = ((sm_mask >> (e >> 3)) & 1u) ? static_cast<int>((sm_k0 >> (4 * (e >> 3))) & 15u) : 8;
+              const int k = e & 7, cut = sm_cut[e >> 3];
               const float base = (k >= cut) ? 0.f : off[e >> 3];
               if (excl) return (k == 0 || k == cut) ? (base + 0.f) : (vv[e - 1] + base);
               return vv[e] + base;
@@ -4139,6 +4141,8 @@ static bool splitm_enabled() {
 // 75 %); fp16 output keeps ROWSEG (SPLITM 44-52 %), gcd 2 / 4 keep GENERAL
 // (87 % vs 76-80 %)
 static bool splitm_wins(long long s, int out_esize) {
+  const char* e = getenv("TC_SPLITM");
+  if (e && e[0] == '2') return s >= kSplitMMin && s < kRow && gcd_ll(s, 64) <= 4;  // probe: always
   return splitm_enabled() && out_esize == 4 && (s & 1) && s >= 11 && s < kRow;
 }
 // largest segment whose range-entry carry a bounded scan recomputes (above:
