@@ -628,19 +628,28 @@ def run_extras(args, x, dev, world, rank, barrier, max_over_ranks, peak):
     del xb
     rows = []
     y = torch.empty(n, dtype=torch.float16, device=dev)
-    for s in (3, 7, 17, 48, 300, 1000, 100000):
+    y32 = torch.empty(n, dtype=torch.float32, device=dev)
+    for s in (3, 7, 17, 33, 48, 63, 300, 1000, 4097, 100000, 100001):
         o = torch.empty(-(-n // s), dtype=torch.float16, device=dev)
         ms = _time_op(lambda: D.seg_reduce(x, s, torch.float16, out=o), reps, 2, stream,
                       barrier, max_over_ranks)
         b = reduce_bytes(n, s)
         ms2 = _time_op(lambda: D.seg_scan(x, s, torch.float16, out=y), reps, 2, stream,
                        barrier, max_over_ranks)
+        ms3 = _time_op(lambda: D.seg_scan(x, s, torch.float32, out=y32), reps, 2, stream,
+                       barrier, max_over_ranks)
         rows.append({"seg": s, "reduce_ms": round(ms, 4),
                      "reduce_frac": round(b / ms / 1e6 / peak, 4), "scan_ms": round(ms2, 4),
-                     "scan_frac": round(4 * n / ms2 / 1e6 / peak, 4)})
-    out["non_pow2_segments"] = {"workload": "segmented reduce / inclusive scan, 2^30 fp16, "
-                                            "fp16 out, ragged last segment", "rows": rows}
-    del y
+                     "scan_frac": round(4 * n / ms2 / 1e6 / peak, 4),
+                     "scan_f32_ms": round(ms3, 4),
+                     "scan_f32_frac": round(6 * n / ms3 / 1e6 / peak, 4),
+                     "modes": {"reduce": D.plan_info("reduce", n, s)[0],
+                               "scan_f16": D.plan_info("scan", n, s)[0],
+                               "scan_f32": D.plan_info("scan", n, s, torch.float32)[0]}})
+    out["non_pow2_segments"] = {"workload": "segmented reduce (fp16 out) / inclusive scan (fp16 "
+                                            "and fp32 out), 2^30 fp16, ragged last segment",
+                                "rows": rows}
+    del y, y32
     # irregular (CSR-offset) segments: geometric lengths
     rows = []
     y = torch.empty(n, dtype=torch.float32, device=dev)

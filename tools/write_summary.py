@@ -34,7 +34,9 @@ L.append(f"| full exclusive scan 2^33 -> fp32 | {fs['ms']} | {fs['gbs_per_gpu_al
 for row in ex["reduce_bf16_input"]["rows"]:
     L.append(f"| seg reduce bf16 in, s={row['seg']} | {row['ms']} | {row['gbs_per_gpu']} | {100*row['frac']:.1f} |")
 for row in ex["non_pow2_segments"]["rows"]:
-    L.append(f"| non-pow2 s={row['seg']} reduce / scan (fp16 out) | {row['reduce_ms']} / {row['scan_ms']} | | {100*row['reduce_frac']:.1f} / {100*row['scan_frac']:.1f} |")
+    m = row.get("modes", {})
+    f32 = f" / {100*row['scan_f32_frac']:.1f} (f32 out)" if "scan_f32_frac" in row else ""
+    L.append(f"| non-pow2 s={row['seg']} reduce / scan (fp16 out){' / scan (fp32 out)' if f32 else ''} {m} | {row['reduce_ms']} / {row['scan_ms']} | | {100*row['reduce_frac']:.1f} / {100*row['scan_frac']:.1f}{f32} |")
 for row in ex["irregular_segments"]["rows"]:
     L.append(f"| irregular (CSR) mean {row['mean_seg']} ({row['nseg']} segs) reduce / scan, fp32 out | {row['reduce_ms']} / {row['scan_ms']} | | {100*row['reduce_frac']:.1f} / {100*row['scan_frac']:.1f} |")
 bn = ex["batch_norm_stats"]
