@@ -2637,6 +2637,7 @@ struct RsParams {
   void* out;
   long long n, s, L, R, nblk;  // elements, segment, row length, rows, 128-row blocks
   int k, nchunk;               // segments per row, 64-column chunks per row
+  int evict_normal;            // L2 policy of the input loads (0: evict-first)
 };
 
 struct RsMisc {
@@ -2722,7 +2723,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint64_t pol = ptx::policy_evict_first();
+      const uint64_t pol = p.evict_normal ? ptx::policy_evict_normal() : ptx::policy_evict_first();
       int i = 0;
       for (long long b = b_begin; b < b_end; ++b)
         for (int c = 0; c < nch; ++c, ++i) {
@@ -2890,6 +2891,7 @@ struct RssParams {
   void* out;
   long long n, s, L, R, nblk;
   int nchunk, exclusive;
+  int evict_normal;  // L2 policy of the input loads (0: evict-first)
 };
 
 template <typename OutT>
@@ -2958,7 +2960,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint64_t pol = ptx::policy_evict_first();
+      const uint64_t pol = p.evict_normal ? ptx::policy_evict_normal() : ptx::policy_evict_first();
       int i = 0;
       for (long long b = b_begin; b < b_end; ++b)
         for (int c = 0; c < nch; ++c, ++i) {
@@ -3610,7 +3612,8 @@ static DevInfo dev_info(int dev) {
 
 static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base,
                      long long rows, int box_cols, long long row_len = kRow,
-                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B,
+                     CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(row_len), static_cast<cuuint64_t>(rows)};
@@ -3619,8 +3622,46 @@ static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int esize, const vo
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+// L2 handling of the strided [R x L] row-segment input view.  With more than
+// one 64-column chunk per row, each box reads 128 rows of 128 B at a 2L-byte
+// pitch, and a pitch that is not a multiple of 128 B makes every piece
+// straddle two 128-B lines whose other half belongs to the row's next chunk,
+// loaded a few boxes later: evict-first loads drop those halves and they are
+// read from HBM twice.  Measured on B200 (2^30 fp16, % of copy bandwidth;
+// tools/probe_modes.py with PROBE_AB_R=multi, profiles/r02/rowseg_l2/):
+//   (promotion, policy)          (256 B, first) (none, first) (256 B, normal)
+//   reduce s = 9 / 17 / 33 f16        79 / 82 / 82   84 / 86 / 82   98 / 97 / 94
+//   reduce s = 3 / 7 (one chunk)      88 / 80        91 / 82        59 / 51
+//   reduce s = 49 / 100 / 300 f16     92 / 98 / 94   87 / 91 / 86   80 / 96 / 82
+//   scan f16 s = 3 / 17 / 33          81 / 69 / 67   86 / 72 / 71   89 / 82 / 82
+// so: one chunk per row (contiguous boxes) -> no promotion, evict-first;
+// scans and reduces with s < 48 -> 256-B promotion, evict-normal; reduces
+// with s >= 48 -> 256-B promotion, evict-first.  TC_RS_PROMO (0 / 64 / 128 /
+// 256) and TC_RS_EVICT (0 / 1) override (A/B switches).
+struct RsL2 {
+  CUtensorMapL2promotion promo;
+  int evict_normal;
+};
+static RsL2 rs_l2(bool scan, long long s, int nchunk) {
+  int promo = 256, normal = 0;
+  if (nchunk <= 1) {
+    promo = 0;
+  } else if (scan || s < 48) {
+    normal = 1;
+  }
+  if (const char* e = getenv("TC_RS_PROMO")) promo = atoi(e);
+  if (const char* e = getenv("TC_RS_EVICT")) normal = atoi(e) == 1 ? 1 : 0;
+  RsL2 r;
+  r.promo = promo == 0     ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+            : promo == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+            : promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                           : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  r.evict_normal = normal;
+  return r;
 }
 
 static long long gcd_ll(long long a, long long b) {
@@ -3670,10 +3711,12 @@ static bool splitm_wins(long long s, int out_esize);
 constexpr long long kSplitMMin = 9;  // >= 9: at most one start per granule of 8
 static int rowseg_scan_k(long long s, long long n, int out_esize) {
   if (s < 2 || s >= n || s >= kRow) return 0;
-  if (split_enabled() && splitm_wins(s, out_esize)) return 0;  // MODE_SPLITM
+  const char* all = getenv("TC_RSS_ALL");  // probe switch: ROWSEG for every s < 64 with gcd <= 2
+  const bool force = all && atoi(all) == 1;
+  if (!force && split_enabled() && splitm_wins(s, out_esize)) return 0;  // MODE_SPLITM
   const long long g = gcd_ll(s, 64);
   if (g > 2) return 0;
-  if (out_esize == 4 && (g == 2 || s > 9)) return 0;
+  if (!force && out_esize == 4 && (g == 2 || s > 9)) return 0;
   int best = 0;
   double best_cost = 0.0;
   for (long long k = 8 / gcd_ll(s, 8); k * s <= 64LL * kRssMaxChunks; k *= 2) {
@@ -3896,7 +3939,7 @@ static int launch_rowseg_k(const RsParams& p0, void* ws, cudaStream_t st) {
   const char* wsb = reinterpret_cast<const char*>(ws);
   const bool ok = p.R > 0
       ? make_map(&tin, p.in_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                 2, p.x, p.R, kRow, p.L)
+                 2, p.x, p.R, kRow, p.L, CU_TENSOR_MAP_SWIZZLE_128B, rs_l2(false, p.s, p.nchunk).promo)
       : make_map(&tin, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, wsb + kWsZeroRow, 1, kRow);
   if (!ok) {
     set_err("cuTensorMapEncodeTiled (row-segment input) failed%s%lld", "", 0);
@@ -3972,7 +4015,7 @@ static int launch_rowseg_scan(const RssParams& p0, void* ws, cudaStream_t st) {
   bool ok;
   if (p.R > 0) {
     ok = make_map(&tin, p.in_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                  2, p.x, p.R, kRow, p.L) &&
+                  2, p.x, p.R, kRow, p.L, CU_TENSOR_MAP_SWIZZLE_128B, rs_l2(true, p.s, p.nchunk).promo) &&
          (fp16 ? make_map(&tout, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, p.out, p.R, kRow, p.L)
                : make_map(&tout, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.out, p.R, 32, p.L));
   } else {
@@ -4263,6 +4306,7 @@ int tc_seg_reduce_ex(const void* x, int in_dtype, int64_t n, int64_t seg, void* 
     rp.R = n / rp.L;
     rp.nblk = (rp.R + kTileRows - 1) / kTileRows;
     rp.nchunk = static_cast<int>((rp.L + kRow - 1) / kRow);
+    rp.evict_normal = rs_l2(false, seg, rp.nchunk).evict_normal;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     return out_dtype == TC_F16   ? launch_rowseg<__half>(rp, ws, st)
            : out_dtype == TC_F32 ? launch_rowseg<float>(rp, ws, st)
@@ -4324,6 +4368,7 @@ int tc_seg_scan_ex(const void* x, int in_dtype, int64_t n, int64_t seg, void* ou
       rp.nblk = (rp.R + kTileRows - 1) / kTileRows;
       rp.nchunk = static_cast<int>((rp.L + kRow - 1) / kRow);
       rp.exclusive = exclusive ? 1 : 0;
+      rp.evict_normal = rs_l2(true, seg, rp.nchunk).evict_normal;
       cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
       return out_dtype == TC_F16 ? launch_rowseg_scan<__half>(rp, ws, st)
                                  : launch_rowseg_scan<float>(rp, ws, st);
