@@ -1800,7 +1800,63 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
             if constexpr (MODE == MODE_GSCR) {
               if (rit == 0) misc->tile_o[par] = qdiv;  // first segment ending in this tile (row 0)
             }
-            if (dl >= GR && row != p.rows_full) {
+            if constexpr (MODE == MODE_SPLIT) {
+              // MODE_SPLIT (s > 64, gcd(s, 64) <= 4): granules of 8 and at most
+              // one segment end per row, at column rem0 (element granularity).
+              // Whole granules go to the head or the tail; the granule the end
+              // splits is re-summed from its 8 raw elements (sp_raw: the
+              // tile's SMEM stage, read above), so head and tail stay forward
+              // fp32 sums of their own segment's elements.
+              const long long rowpos = row * kRow;
+              if (rowpos + kRow < p.n) {
+                const int ee = rem0 < kRow ? static_cast<int>(rem0) : kRow;  // end column (64: none)
+                const int ge = (ee + 1) >> 3, o = (ee + 1) & 7;  // split granule, elements before the split
+                const int gt = o == 0 ? ge : ge + 1;            // first whole granule of the tail
+                float hs = 0.f, ts = 0.f;
+  #pragma unroll
+                for (int j = 0; j < GR; ++j) {
+                  hs += j < ge ? gs[j] : 0.f;
+                  ts += j >= gt ? gs[j] : 0.f;
+                }
+                seen = ee < kRow ? 1 : 0;
+                if (seen && o != 0) {
+                  const uint32_t* hw = reinterpret_cast<const uint32_t*>(&sp_raw);
+                  float hp = 0.f, tp = 0.f;
+  #pragma unroll
+                  for (int k = 0; k < 8; ++k) {
+                    const uint32_t b = (hw[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+                    const float xk = p.in_bf16 ? __uint_as_float(b << 16)
+                                               : __half2float(__ushort_as_half(static_cast<unsigned short>(b)));
+                    hp += k < o ? xk : 0.f;
+                    tp += k < o ? 0.f : xk;
+                  }
+                  hs += hp;
+                  ts = tp + ts;
+                }
+                head = hs;
+                run = seen ? ts : hs;
+              } else {
+                // the row holding the input's last element (or past it): walk
+                // its elements from HBM; its ends are the regular one (column
+                // rem0) and the input's last element
+                const int ee = rem0 < kRow ? static_cast<int>(rem0) : kRow;
+                long long sg = seg0;
+                for (int k = 0; k < kRow && rowpos + k < p.n; ++k) {
+                  const long long e = rowpos + k;
+                  run += in_to_float(p.x, e, p.in_bf16 != 0);
+                  if (k == ee || e == p.n - 1) {
+                    if (!seen) {
+                      head = run;
+                      seen = 1;
+                    } else {
+                      out[sg] = cvt_out<OutT>(run);  // the ragged last segment, wholly in this row
+                    }
+                    ++sg;
+                    run = 0.f;
+                  }
+                }
+              }
+            } else if (dl >= GR && row != p.rows_full) {
               // a full row that does not hold the input's last granule
               if constexpr (MODE == MODE_GSCR) {
                 // many ends per row (2m < GR): ends at e0 < m, e0 + m, ...;
@@ -2444,6 +2500,11 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
             // closed inside the range (the row holding its end offset
             // closes it), and it is the end offset itself in the last range
             e1.seg = (kc - 1 < p.nseg) ? kc - 1 : -1LL;
+          } else if constexpr (MODE == MODE_SPLIT) {
+            // element granularity (p.m = seg)
+            const long long le = (t_end * kTileElems < p.n ? t_end * kTileElems : p.n) - 1;
+            const bool closed = ((le + 1) % p.m == 0) || (le == p.n - 1);
+            e1.seg = closed ? -1LL : le / p.m;
           } else {
             const long long lg_end = t_end * static_cast<long long>(kTileRows) * GR;
             const long long lg = (lg_end < p.qlast + 1 ? lg_end : p.qlast + 1) - 1;
@@ -3680,6 +3741,11 @@ static long long gcd_ll(long long a, long long b) {
 // fewest 64-column chunks per element (a partly filled last chunk costs a
 // whole chunk's pipeline slot; measured on B200: rows of 40 elements run at
 // ~42 % of copy bandwidth, whole 64-column chunks at ~90 %).
+// TC_RS_TIE=1: among equally filled layouts take the longest rows (A/B switch)
+static bool rs_tie_longer() {
+  const char* e = getenv("TC_RS_TIE");
+  return e && atoi(e) == 1;
+}
 static int rowseg_k(long long s, long long n, int out_esize) {
   if (s < 2 || s >= n) return 0;
   if (gcd_ll(s, 64) > 8) return 0;  // >= 16-element granules: the GENERAL kernel is as fast
@@ -3691,7 +3757,8 @@ static int rowseg_k(long long s, long long n, int out_esize) {
     const long long nn = k < 16 ? 16 : k;
     if (nch * nn * 128 > static_cast<long long>(kRsMaxB)) break;
     const double cost = static_cast<double>(nch) / static_cast<double>(L);
-    if (best == 0 || cost < best_cost * (1.0 - 1e-9)) {
+    if (best == 0 || cost < best_cost * (1.0 - 1e-9) ||
+        (rs_tie_longer() && cost < best_cost * (1.0 + 1e-9))) {
       best = static_cast<int>(k);
       best_cost = cost;
     }
@@ -4121,8 +4188,7 @@ static LaunchFn pick(int gr, int mode) {
       return nullptr;
     case MODE_IRREG: return gr == 1 ? &launch<OP, 1, MODE_IRREG, OutT> : nullptr;
     case MODE_SPLIT:
-      if constexpr (OP == OP_SCAN) return gr == 8 ? &launch<OP, 8, MODE_SPLIT, OutT> : nullptr;
-      return nullptr;
+      return gr == 8 ? &launch<OP, 8, MODE_SPLIT, OutT> : nullptr;
     case MODE_SPLITM:
       if constexpr (OP == OP_SCAN) return gr == 8 ? &launch<OP, 8, MODE_SPLITM, OutT> : nullptr;
       return nullptr;
@@ -4173,6 +4239,11 @@ static int common_checks(const void* x, long long n, long long seg, const void* 
 // Segment geometry -> granules, carry mode and per-mode constants.
 static bool split_enabled() {
   const char* e = getenv("TC_SPLIT");  // tuning / A-B switch
+  return !(e && e[0] == '0');
+}
+constexpr long long kSplitReduceMin = kTileElems + kTileElems / 2;  // SPLIT reduce from here on
+static bool split_reduce_enabled() {
+  const char* e = getenv("TC_SPLIT_REDUCE");  // A/B switch: GENERAL (one-element granules) instead
   return !(e && e[0] == '0');
 }
 static bool splitm_enabled() {
@@ -4243,6 +4314,20 @@ static Params make_params(const void* x, long long n, long long seg, void* out, 
     p.step_div = kTileElems / seg;
     p.step_mod = kTileElems % seg;
   }
+  if (op == TC_OP_REDUCE && mode == MODE_GENERAL && g <= 4 && seg >= kSplitReduceMin &&
+      split_enabled() && split_reduce_enabled()) {
+    // the same for reduces: granules of 8, at most one end per row, the
+    // granule it splits re-summed from its raw elements.  Measured on B200
+    // (2^30 fp16, % of copy, SPLIT vs GENERAL with one-element granules):
+    // s = 4097 76 / 82, 8193 77 / 81, 12289 85 / 83, 32769 89 / 84,
+    // 65537 91 / 84, 100001 92 / 85 -- below ~1.5 ends per tile the split
+    // rows' divergent raw pass holds the tile's pair-scan barrier
+    mode = MODE_SPLIT;
+    gr = 8;
+    p.m = seg;
+    p.step_div = kTileElems / seg;
+    p.step_mod = kTileElems % seg;
+  }
   if (op == TC_OP_SCAN && (mode == MODE_TILES || mode == MODE_GENERAL) &&
       (seg > prepass_max(gr) || scan_carry))
     mode = MODE_CHUNK;
@@ -4262,7 +4347,8 @@ static Params make_params(const void* x, long long n, long long seg, void* out, 
   if (op == TC_OP_REDUCE && mode == MODE_GENERAL && 2 * p.m < gr) mode = MODE_GSCR;
   *mode_out = mode;
   p.need_fixup = (op == TC_OP_REDUCE &&
-                  (mode == MODE_TILES || mode == MODE_GENERAL || mode == MODE_GSCR) &&
+                  (mode == MODE_TILES || mode == MODE_GENERAL || mode == MODE_GSCR ||
+                   mode == MODE_SPLIT) &&
                   (kTileElems % seg != 0))
                      ? 1
                      : 0;

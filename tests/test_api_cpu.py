@@ -265,7 +265,9 @@ def test_plan_info_modes():
     assert mode == "ROWSEG" and L % 3 == 0 and (2 * L) % 16 == 0
     mode, L = D.plan_info("reduce", n, 3, torch.float32)
     assert mode == "ROWSEG" and (L // 3) * 4 <= 64
-    assert D.plan_info("reduce", n, 100001)[0] == "GENERAL"
+    assert D.plan_info("reduce", n, 100001)[0] == "SPLIT"
+    assert D.plan_info("reduce", n, 1000)[0] == "GENERAL"  # gcd 8: whole granules
+    assert D.plan_info("reduce", n, 4097)[0] == "GENERAL"  # SPLIT only from 1.5 tiles per segment
     assert D.plan_info("scan", n, n)[0] == "CHUNK"
     assert D.plan_info("scan", n, 4096, carry_in=True)[0] == "CHUNK"
     assert D.plan_info("scan", n, 17)[0] == "ROWSEG"

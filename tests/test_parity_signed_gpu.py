@@ -43,10 +43,12 @@ N = (1 << 22) + 1234  # ragged: not a multiple of 64, 8192 or any segment size
 
 # segment sizes by kernel mode (tc_collectives.cu make_params):
 #   LOCAL s | 64; ROWS 64 * 2^k <= 8192; TILES 8192 * k; GENERAL (incl. the
-#   one/two-end select sums: 48, 100, 300, 1000, 65, 100001); GSCR (many ends
-#   per row: 3, 7, 17, 24, 63, 12, 20)
+#   one/two-end select sums: 48, 1000, 127, 129, 4097); GSCR (many ends per
+#   row); ROWSEG (gcd(s, 64) <= 8 with whole segments per TMA row: 3, 7, 12,
+#   17, 20, 24, 63, 65, 100, 300); SPLIT (s >= 12288, gcd(s, 64) <= 4:
+#   16411, 100001, 524292, 1000003)
 REDUCE_SEGS = [1, 2, 16, 64, 256, 8192, 16384, 24576, 3, 7, 12, 17, 20, 24, 63, 48, 65, 100,
-               300, 1000, 100001, N]
+               127, 129, 4097, 16411, 524292, 1000003, 300, 1000, 100001, N]
 #   scans: LOCAL / ROWS / TILES / GENERAL as above; ROWSEG (s < 9, gcd(s, 64)
 #   <= 2, fp16 out: 3, 6, 9, 17, 33, 63; fp32 out s <= 9); SPLITM (fp32 out, odd
 #   11 <= s < 64: 17, 33, 63); SPLIT (s >= 64, gcd(s, 64) <= 4, up to

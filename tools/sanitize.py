@@ -45,8 +45,9 @@ def main():
 
 
 def run_reduce(x, xd, n, done):
-    # reduce: LOCAL 16, ROWS 256, TILES 16384 (fixup: 8192*3), GENERAL 300 / 48 / 100, GSCR 17 / 3
-    for s in (16, 256, 16384, 8192 * 3, 300, 48, 100, 17, 3, 1000, n):
+    # reduce: LOCAL 16, ROWS 256, TILES 16384 (fixup: 8192*3), GENERAL 300 / 48 / 100, GSCR 17 / 3,
+    # SPLIT 16411 / 100001 (split granule from the held SMEM stage, cross-CTA fixup)
+    for s in (16, 256, 16384, 8192 * 3, 300, 48, 100, 17, 3, 1000, 16411, 100001, n):
         for dt, npdt in ((torch.float16, np.float16), (torch.float32, np.float32),
                          (torch.float64, np.float64)):
             got = D.seg_reduce(xd, s, dt).cpu().numpy()
