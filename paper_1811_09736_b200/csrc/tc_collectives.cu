@@ -1808,33 +1808,46 @@ __global__ void __launch_bounds__((Cfg<OP, GR, MODE, OutT>::THREADS), (Cfg<OP, G
               // tile's SMEM stage, read above), so head and tail stay forward
               // fp32 sums of their own segment's elements.
               const long long rowpos = row * kRow;
-              if (rowpos + kRow < p.n) {
+              const bool regular = rowpos + kRow < p.n;
+              // warp-uniform: does any regular row of this warp hold an end?
+              const bool any_end = __any_sync(kFull, regular && rem0 < kRow);
+              if (regular) {
                 const int ee = rem0 < kRow ? static_cast<int>(rem0) : kRow;  // end column (64: none)
-                const int ge = (ee + 1) >> 3, o = (ee + 1) & 7;  // split granule, elements before the split
-                const int gt = o == 0 ? ge : ge + 1;            // first whole granule of the tail
-                float hs = 0.f, ts = 0.f;
-  #pragma unroll
-                for (int j = 0; j < GR; ++j) {
-                  hs += j < ge ? gs[j] : 0.f;
-                  ts += j >= gt ? gs[j] : 0.f;
-                }
                 seen = ee < kRow ? 1 : 0;
-                if (seen && o != 0) {
-                  const uint32_t* hw = reinterpret_cast<const uint32_t*>(&sp_raw);
-                  float hp = 0.f, tp = 0.f;
+                // pairwise trees (short dependency chains): the row total, and
+                // only in warps holding an end the head / tail pieces
+                const float total = ((gs[0] + gs[1]) + (gs[2] + gs[3])) + ((gs[4] + gs[5]) + (gs[6] + gs[7]));
+                run = total;
+                if (any_end) {
+                  const int ge = (ee + 1) >> 3, o = (ee + 1) & 7;  // split granule, elements before the split
+                  const int gt = o == 0 ? ge : ge + 1;            // first whole granule of the tail
+                  float hv[8], tv8[8];
   #pragma unroll
-                  for (int k = 0; k < 8; ++k) {
-                    const uint32_t b = (hw[k >> 1] >> (16 * (k & 1))) & 0xffffu;
-                    const float xk = p.in_bf16 ? __uint_as_float(b << 16)
-                                               : __half2float(__ushort_as_half(static_cast<unsigned short>(b)));
-                    hp += k < o ? xk : 0.f;
-                    tp += k < o ? 0.f : xk;
+                  for (int j = 0; j < GR; ++j) {
+                    hv[j] = j < ge ? gs[j] : 0.f;
+                    tv8[j] = j >= gt ? gs[j] : 0.f;
                   }
-                  hs += hp;
-                  ts = tp + ts;
+                  float hs = ((hv[0] + hv[1]) + (hv[2] + hv[3])) + ((hv[4] + hv[5]) + (hv[6] + hv[7]));
+                  float ts = ((tv8[0] + tv8[1]) + (tv8[2] + tv8[3])) + ((tv8[4] + tv8[5]) + (tv8[6] + tv8[7]));
+                  if (o != 0) {
+                    const uint32_t* hw = reinterpret_cast<const uint32_t*>(&sp_raw);
+                    float xh[8], xt[8];
+  #pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                      const uint32_t bb = (hw[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+                      const float xk = p.in_bf16 ? __uint_as_float(bb << 16)
+                                                 : __half2float(__ushort_as_half(static_cast<unsigned short>(bb)));
+                      xh[k] = k < o ? xk : 0.f;
+                      xt[k] = k < o ? 0.f : xk;
+                    }
+                    hs += ((xh[0] + xh[1]) + (xh[2] + xh[3])) + ((xh[4] + xh[5]) + (xh[6] + xh[7]));
+                    ts = ((xt[0] + xt[1]) + (xt[2] + xt[3])) + ((xt[4] + xt[5]) + (xt[6] + xt[7])) + ts;
+                  }
+                  if (seen) {
+                    head = hs;
+                    run = ts;
+                  }
                 }
-                head = hs;
-                run = seen ? ts : hs;
               } else {
                 // the row holding the input's last element (or past it): walk
                 // its elements from HBM; its ends are the regular one (column
@@ -3699,19 +3712,21 @@ static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int esize, const vo
 //   reduce s = 3 / 7 (one chunk)      88 / 80        91 / 82        59 / 51
 //   reduce s = 49 / 100 / 300 f16     92 / 98 / 94   87 / 91 / 86   80 / 96 / 82
 //   scan f16 s = 3 / 17 / 33          81 / 69 / 67   86 / 72 / 71   89 / 82 / 82
+//   reduce s = 49 / 63 / 65 f32 (twice)  74 / 78 / 77   76 / 78 / 77   82 / 88 / 86
 // so: one chunk per row (contiguous boxes) -> no promotion, evict-first;
-// scans and reduces with s < 48 -> 256-B promotion, evict-normal; reduces
-// with s >= 48 -> 256-B promotion, evict-first.  TC_RS_PROMO (0 / 64 / 128 /
+// scans, reduces with s < 48 and fp32 / fp64-output reduces -> 256-B
+// promotion, evict-normal; fp16-output reduces with s >= 48 -> 256-B
+// promotion, evict-first.  TC_RS_PROMO (0 / 64 / 128 /
 // 256) and TC_RS_EVICT (0 / 1) override (A/B switches).
 struct RsL2 {
   CUtensorMapL2promotion promo;
   int evict_normal;
 };
-static RsL2 rs_l2(bool scan, long long s, int nchunk) {
+static RsL2 rs_l2(bool scan, long long s, int nchunk, int out_esize = 2) {
   int promo = 256, normal = 0;
   if (nchunk <= 1) {
     promo = 0;
-  } else if (scan || s < 48) {
+  } else if (scan || s < 48 || out_esize >= 4) {
     normal = 1;
   }
   if (const char* e = getenv("TC_RS_PROMO")) promo = atoi(e);
@@ -4243,8 +4258,12 @@ static bool split_enabled() {
 }
 constexpr long long kSplitReduceMin = kTileElems + kTileElems / 2;  // SPLIT reduce from here on
 static bool split_reduce_enabled() {
-  const char* e = getenv("TC_SPLIT_REDUCE");  // A/B switch: GENERAL (one-element granules) instead
+  const char* e = getenv("TC_SPLIT_REDUCE");  // A/B switch: 0 = GENERAL (one-element granules) instead
   return !(e && e[0] == '0');
+}
+static bool split_reduce_forced() {
+  const char* e = getenv("TC_SPLIT_REDUCE");  // probe switch: 2 = SPLIT for every s > 64
+  return e && e[0] == '2';
 }
 static bool splitm_enabled() {
   const char* e = getenv("TC_SPLITM");  // tuning / A-B switch
@@ -4314,14 +4333,15 @@ static Params make_params(const void* x, long long n, long long seg, void* out, 
     p.step_div = kTileElems / seg;
     p.step_mod = kTileElems % seg;
   }
-  if (op == TC_OP_REDUCE && mode == MODE_GENERAL && g <= 4 && seg >= kSplitReduceMin &&
-      split_enabled() && split_reduce_enabled()) {
+  if (op == TC_OP_REDUCE && mode == MODE_GENERAL && g <= 4 && seg > kRow &&
+      (seg >= kSplitReduceMin || split_reduce_forced()) && split_enabled() &&
+      split_reduce_enabled()) {
     // the same for reduces: granules of 8, at most one end per row, the
     // granule it splits re-summed from its raw elements.  Measured on B200
     // (2^30 fp16, % of copy, SPLIT vs GENERAL with one-element granules):
-    // s = 4097 76 / 82, 8193 77 / 81, 12289 85 / 83, 32769 89 / 84,
-    // 65537 91 / 84, 100001 92 / 85 -- below ~1.5 ends per tile the split
-    // rows' divergent raw pass holds the tile's pair-scan barrier
+    // s = 127 77 / 82, 4097 78 / 81, 8193 79 / 82, 12289 93 / 83,
+    // 32769 101 / 84, 100001 93 / 85 -- with one or more ends per tile the
+    // split rows' extra pass holds the tile's pair-scan barrier
     mode = MODE_SPLIT;
     gr = 8;
     p.m = seg;
@@ -4392,7 +4412,7 @@ int tc_seg_reduce_ex(const void* x, int in_dtype, int64_t n, int64_t seg, void* 
     rp.R = n / rp.L;
     rp.nblk = (rp.R + kTileRows - 1) / kTileRows;
     rp.nchunk = static_cast<int>((rp.L + kRow - 1) / kRow);
-    rp.evict_normal = rs_l2(false, seg, rp.nchunk).evict_normal;
+    rp.evict_normal = rs_l2(false, seg, rp.nchunk, out_es).evict_normal;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     return out_dtype == TC_F16   ? launch_rowseg<__half>(rp, ws, st)
            : out_dtype == TC_F32 ? launch_rowseg<float>(rp, ws, st)
