@@ -2939,9 +2939,15 @@ __global__ void __launch_bounds__(kThreads, 2)
 // of n - R L < L elements is scanned in fp64 by the last CTA.
 constexpr int kRssStages = 4;
 constexpr int kRssAcc = 8;  // 8 x 64 TMEM columns: 1 CTA / SM
-constexpr int kRssMaxChunks = 10;
+// chunks per row: B matrices of 8 KB each between the input ring and the
+// output staging (fp16 output: 16 fit the 227-KB budget, fp32: 10)
+constexpr int kRssMaxChunks = 16;
+__host__ __device__ constexpr int rss_max_chunks(int out_esize) { return out_esize == 2 ? 16 : 10; }
 constexpr uint32_t kRssOffB = kRssStages * kTileBytes;
-constexpr uint32_t kRssOffOut = kRssOffB + kRssMaxChunks * 8192;
+template <typename OutT>
+__host__ __device__ constexpr uint32_t rss_off_out() {
+  return kRssOffB + rss_max_chunks(static_cast<int>(sizeof(OutT))) * 8192;
+}
 
 struct RssMisc {
   uint64_t full[kRssStages];
@@ -2956,7 +2962,7 @@ struct RssMisc {
 
 template <typename OutT>
 constexpr uint32_t rss_smem() {
-  return kRssOffOut + 2 * kTileElems * sizeof(OutT) + sizeof(RssMisc) + 1024;
+  return rss_off_out<OutT>() + 2 * kTileElems * sizeof(OutT) + sizeof(RssMisc) + 1024;
 }
 
 struct RssParams {
@@ -2975,7 +2981,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr uint32_t kOutBytes = kTileElems * sizeof(OutT);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-  RssMisc* misc = reinterpret_cast<RssMisc*>(smem + kRssOffOut + 2 * kOutBytes);
+  RssMisc* misc = reinterpret_cast<RssMisc*>(smem + rss_off_out<OutT>() + 2 * kOutBytes);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const long long b_begin = p.nblk * blockIdx.x / gridDim.x;
@@ -3116,7 +3122,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // stage (swizzled, as the output tensor map's SW128 box) and store
         if (leader) ptx::bulk_wait_read<1>();
         ptx::named_bar_sync(kEpiBar, kEpiThreads);
-        uint8_t* stg = smem + kRssOffOut + par * kOutBytes;
+        uint8_t* stg = smem + rss_off_out<OutT>() + par * kOutBytes;
         const uint32_t rb = static_cast<uint32_t>(rit) * 128u;
         const uint32_t sw = static_cast<uint32_t>(rit & 7);
         if constexpr (sizeof(OutT) == 2) {
@@ -3782,7 +3788,7 @@ static int rowseg_k(long long s, long long n, int out_esize) {
 }
 
 // Segments per row for the MODE_ROWSEG scan (0 = not applicable): rows of
-// L = k s <= 64 kRssMaxChunks elements, k a power of two times 8 / gcd(s, 8),
+// L = k s <= 64 rss_max_chunks elements, k a power of two times 8 / gcd(s, 8),
 // the fewest chunks per element.  Only where it beats the granule scan
 // (measured on B200, 2^30 fp16, % of copy bandwidth): s < 64 (larger s run
 // as MODE_SPLIT), gcd(s, 64) <= 2 (gcd 4: GENERAL 88 % vs 61-83 %); with
@@ -3801,12 +3807,23 @@ static int rowseg_scan_k(long long s, long long n, int out_esize) {
   if (!force && out_esize == 4 && (g == 2 || s > 9)) return 0;
   int best = 0;
   double best_cost = 0.0;
-  for (long long k = 8 / gcd_ll(s, 8); k * s <= 64LL * kRssMaxChunks; k *= 2) {
+  // among layouts of equal cost, rows of whole 32-B sectors (L % 16 == 0):
+  // a row pitch ending mid-sector makes every strided box write partial
+  // sectors (measured, fp16 out: s = 23 / 29 / 31 / 39 80 / 77 / 80 / 78 ->
+  // 85 / 82 / 82 / 79 %); TC_RSS_ALIGN32=0 turns the preference off
+  const char* al = getenv("TC_RSS_ALIGN32");
+  const bool prefer_aligned = !(al && al[0] == '0');
+  const long long lmax = 64LL * rss_max_chunks(out_esize);
+  bool best_al = false;
+  for (long long k = 8 / gcd_ll(s, 8); k * s <= lmax; k *= 2) {
     const long long L = k * s;
     const double cost = static_cast<double>((L + kRow - 1) / kRow) / static_cast<double>(L);
-    if (best == 0 || cost < best_cost * (1.0 - 1e-9)) {
+    const bool aligned = prefer_aligned && (L % 16 == 0);
+    if (best == 0 || cost < best_cost * (1.0 - 1e-9) ||
+        (aligned && !best_al && cost < best_cost * (1.0 + 1e-9))) {
       best = static_cast<int>(k);
       best_cost = cost;
+      best_al = aligned;
     }
   }
   return best;
