@@ -268,6 +268,12 @@ def test_plan_info_modes():
     assert D.plan_info("reduce", n, 100001)[0] == "SPLIT"
     assert D.plan_info("reduce", n, 1000)[0] == "GENERAL"  # gcd 8: whole granules
     assert D.plan_info("reduce", n, 4097)[0] == "GENERAL"  # SPLIT only from 1.5 tiles per segment
+    assert D.plan_info("reduce", n, 8193)[0] == "GENERAL"
+    assert D.plan_info("reduce", n, 12289)[0] == "SPLIT"
+    # ROWSEG scan rows (fp16 out): up to 16 chunks, whole 32-B sectors among equal-cost layouts
+    assert D.plan_info("scan", n, 63) == ("ROWSEG", 1008)
+    assert D.plan_info("scan", n, 23) == ("ROWSEG", 368)
+    assert D.plan_info("scan", n, 49) == ("ROWSEG", 784)
     assert D.plan_info("scan", n, n)[0] == "CHUNK"
     assert D.plan_info("scan", n, 4096, carry_in=True)[0] == "CHUNK"
     assert D.plan_info("scan", n, 17)[0] == "ROWSEG"
